@@ -1,0 +1,418 @@
+#!/usr/bin/env python3
+"""Benchmark: fused 3-D Euler inviscid flux on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fvb|reference]
+                    [--config flux3d|cons2prim1d|jacobian3d|axpy] [--prec f64|f32]
+                    [--n POINTS_PER_GPU]
+
+One step = one pass of the hot path over one batch: the fused flux kernel over
+N = 1e8 points per GPU (C3: 3-D, fp64, 5 input planes -> 15 output planes,
+160 algorithmic bytes/point), inputs synthesised on the device by the
+random-access SplitMix64 generator (bit-identical to the reference's host
+generator) and resident in HBM before the clock starts.  Multi-GPU: one
+process per GPU (torchrun), each owning the contiguous global slice
+[r*N, (r+1)*N) -- weak scaling, no collective on the flux path (C4 adds the
+one NCCL allreduce-max of the CFL wave speed).  Timing: CUDA events on the
+launching stream, barrier + synchronize on both sides, max over ranks.
+
+`value` is whole-job points/s with inputs resident; `e2e` is the same metric
+through the host-buffer C-ABI call (fvb_flux_host) from pinned host memory,
+copies included; `cpu_baseline` is the unmodified reference (oracle/_ref) on
+this box's host cores.  `--impl reference` times that reference alone.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "3D Euler flux Gpoints/s and HBM GB/s vs peak at 1/2/4/8 B200 vs CPU ref"
+
+# Algorithmic bytes per point (read + write) and planes.
+CONFIGS = {
+    # name: (dim, n_in, n_out, default N per GPU, description)
+    "flux3d": (3, 5, 15, 100_000_000, "C3: 3D Euler inviscid fluxes, all 3 directions"),
+    "cons2prim1d": (1, 3, 3, 100_000_000, "C2: 1D cons->prim + ideal-gas p + sound speed"),
+    "jacobian3d": (3, 5, 75, 100_000_000, "C4: 3D 5x5 flux Jacobians x3 + CFL max allreduce"),
+    "axpy": (0, 2, 1, 1_000_000, "C1: UETLI y = 0.5*sin(x+y)"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="fvb", choices=["fvb", "reference"])
+    ap.add_argument("--config", default="flux3d", choices=sorted(CONFIGS))
+    ap.add_argument("--prec", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--n", type=int, default=0, help="points per GPU (default: the config's)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=10_000_000,
+                    help="points per reference step (bounded CPU sample)")
+    ap.add_argument("--out", default="", help="also append the JSON line to this file")
+    a = ap.parse_args()
+    if a.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    return a
+
+
+# ---- environment --------------------------------------------------------------------
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profiled_traffic(config, prec):
+    """DRAM bytes per launch from the committed ncu capture, or None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return t.get(f"{config}_{prec}")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8,
+        "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40,
+        "hw_power_brake": 0x80,
+    }
+
+    def __init__(self, index):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception:
+            pass
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.02)
+
+    def __enter__(self):
+        if self._ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._ok:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---- the reference arm (CPU) -----------------------------------------------------------
+
+REF_WHICH = {"flux3d": 0, "cons2prim1d": 1, "jacobian3d": 2, "axpy": 3}
+
+
+def reference_run(cfg_name, prec, steps, warmup, sample, threads):
+    """Time the unmodified reference (oracle/_ref) on the host cores."""
+    import oracle
+
+    R = oracle.reference()
+    if R is None:
+        raise RuntimeError("oracle/_ref/libfvref.so missing (build() on a box with "
+                           "/root/reference)")
+    dim = CONFIGS[cfg_name][0]
+    times = R.time_config(REF_WHICH[cfg_name], max(dim, 1), prec, sample, threads,
+                          warmup + steps)
+    t = times[warmup:]
+    return sample, t
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---- the device arm -----------------------------------------------------------------------
+
+
+def device_run(a, rank, world, local):
+    import torch
+
+    import paper_1809_09851_b200 as fvb
+
+    dim, n_in, n_out, n_default, desc = CONFIGS[a.config]
+    n = a.n or n_default
+    prec = 1 if a.prec == "f64" else 0
+    esize = 8 if prec else 4
+    bytes_per_pt = (n_in + n_out) * esize
+    if a.config == "cons2prim1d":
+        bytes_per_pt = (n_in + n_out) * esize  # rho read, not written: 3R + 3W
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.Stream(device=dev)
+    first = rank * n  # weak scaling: this rank's global slice [r*n, (r+1)*n)
+    dt = torch.float64 if prec else torch.float32
+
+    with torch.cuda.stream(stream):
+        if a.config == "axpy":
+            x = fvb.synth_uniform(n, prec=prec, seed=1, first=first)
+            y = fvb.synth_uniform(n, prec=prec, seed=1, first=world * n + first)
+            ins = [x, y]
+            outs = [y]
+        else:
+            ins = fvb.synth_state(dim, n, prec=prec, seed=0x5EED, first=first)
+            outs = [torch.empty(n, dtype=dt, device=dev) for _ in range(n_out)]
+        lam = torch.empty((), dtype=dt, device=dev)
+        lam_global = torch.empty((), dtype=torch.float64, device=dev)
+
+    def step():
+        if a.config == "flux3d":
+            fvb.flux(ins, dim, out=outs, stream=stream)
+        elif a.config == "cons2prim1d":
+            fvb.cons2prim(ins, dim, out=outs, stream=stream)
+        elif a.config == "jacobian3d":
+            fvb.jacobian(ins, dim, out=outs, lambda_max=lam, stream=stream)
+        else:
+            fvb.axpy_sin(ins[0], ins[1], stream=stream)
+
+    def allreduce():
+        # the path's one real exchange: CFL max over GPUs (NCCL over NVLink)
+        if a.config == "jacobian3d" and dist is not None:
+            with torch.cuda.stream(stream):
+                lam_global.copy_(lam)
+                dist.all_reduce(lam_global, op=dist.ReduceOp.MAX)
+
+    for _ in range(a.warmup):
+        step()
+        allreduce()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    k_start = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    k_end = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(torch.cuda.current_device())
+    with sampler:
+        t0.record(stream)
+        for i in range(a.steps):
+            k_start[i].record(stream)
+            step()
+            k_end[i].record(stream)
+            allreduce()
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    elapsed_ms = t0.elapsed_time(t1)
+    kernel_ms = [s.elapsed_time(e) for s, e in zip(k_start, k_end)]
+    kern_avg = sum(kernel_ms) / len(kernel_ms)
+
+    if dist is not None:
+        tt = torch.tensor([elapsed_ms, kern_avg], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed_ms, kern_avg = tt.tolist()
+
+    # ---- end to end through the host-buffer C-ABI call -----------------------------
+    e2e = None
+    if not a.no_e2e and a.config in ("flux3d", "jacobian3d"):
+        del outs
+        torch.cuda.empty_cache()
+        host_in = [t.cpu().pin_memory() for t in ins]
+        host_out = [torch.empty(n, dtype=dt).pin_memory() for _ in range(n_out)]
+        ctx = fvb.HostContext(local)
+
+        def e2e_step():
+            if a.config == "flux3d":
+                ctx.flux(host_in, dim, host_out)
+            else:
+                ctx.jacobian(host_in, dim, host_out)
+
+        e2e_step()  # warm (staging allocation)
+        if dist is not None:
+            dist.barrier()
+        t_start = time.perf_counter()
+        for _ in range(a.e2e_steps):
+            e2e_step()  # returns after the last D2H copy completed
+        e2e_s = (time.perf_counter() - t_start) / a.e2e_steps
+        if dist is not None:
+            te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            e2e_s = te.item()
+        e2e = {"value": world * n / e2e_s / 1e9, "unit": "Gpoints/s",
+               "h2d_bytes_per_step": world * n * n_in * esize,
+               "d2h_bytes_per_step": world * n * n_out * esize + (8 if a.config == "jacobian3d"
+                                                                  else 0),
+               "ms_per_step": e2e_s * 1e3, "host_memory": "pinned",
+               "path": "fvb_flux_host" if a.config == "flux3d" else "fvb_jacobian_host"}
+        ctx.close()
+
+    # ---- CPU baseline (rank 0, N=1 only) --------------------------------------------
+    cpu = None
+    if not a.no_cpu_baseline and world == 1 and rank == 0:
+        try:
+            threads = cpu_threads()
+            sample = min(n, a.cpu_sample if a.config != "axpy" else n)
+            if a.config == "jacobian3d":
+                sample = min(sample, 2_000_000)
+            pts, times = reference_run(a.config, a.prec, 3, 1, sample, threads)
+            med = statistics.median(times)
+            cpu = {"value": pts / (med * 1e-9) / 1e9, "unit": "Gpoints/s", "cores": threads,
+                   "kind": "reference",
+                   "sample": f"{pts} points of the same workload per rep, median of 3 reps "
+                             f"after 1 JIT warm-up, Backend::parallel(0, {threads})"}
+        except Exception as ex:  # reported, never a substitute for the device number
+            cpu = {"value": None, "unit": "Gpoints/s", "cores": cpu_threads(),
+                   "kind": "reference", "sample": f"unavailable: {ex}"}
+
+    peak, peak_src = measured_peak()
+    achieved = bytes_per_pt * n / (kern_avg * 1e-3) / 1e9
+    ms_per_step = elapsed_ms / a.steps
+    value = world * n / (ms_per_step * 1e-3) / 1e9
+    clocks = sampler.summary()
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "Gpoints/s",
+        "n_gpus": world,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": a.prec,
+        "data": "synthetic (on-device SplitMix64 random_state of acceptance.cpp:214-230, "
+                "seed 0x5eed, bit-identical to the reference generator)",
+        "config": {"workload": desc, "config": a.config, "points_per_gpu": n,
+                   "global_points": world * n, "dim": dim, "precision": a.prec,
+                   "bytes_per_point": bytes_per_pt,
+                   "l2": "inputs larger than L2 (%.1f GB per GPU vs 126 MB)"
+                         % (n * n_in * esize / 1e9),
+                   "parallelism": f"index-range shards x{world}" + (
+                       " + NCCL allreduce-max" if a.config == "jacobian3d" and world > 1 else "")},
+        "hbm_gbs": achieved,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_source": peak_src,
+                     "frac_of_nominal_8000": achieved / 8000.0,
+                     "traffic": profiled_traffic(a.config, a.prec),
+                     "kernel_ms": kern_avg},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": a.steps,
+        "clocks": clocks,
+    }
+    if dist is not None:
+        dist.destroy_process_group()
+    return line
+
+
+def main():
+    a = parse()
+    rank, world, local = dist_env()
+    if a.impl == "reference":
+        if rank != 0:
+            return 0
+        dim, n_in, n_out, n_default, desc = CONFIGS[a.config]
+        threads = cpu_threads()
+        sample = min(a.n or n_default, a.cpu_sample)
+        if a.config == "jacobian3d":
+            sample = min(sample, 2_000_000)
+        # bounded: shrink the per-step sample if the run would exceed ~3 minutes
+        pts, t_probe = reference_run(a.config, a.prec, 1, 1, sample, threads)
+        est = t_probe[0] * 1e-9 * (a.steps + a.warmup)
+        if est > 180:
+            sample = max(100_000, int(sample * 180 / est))
+        pts, times = reference_run(a.config, a.prec, a.steps, a.warmup, sample, threads)
+        ms = statistics.mean(times) * 1e-6
+        value = pts / (ms * 1e-3) / 1e9
+        esize = 8 if a.prec == "f64" else 4
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gpoints/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": a.prec,
+            "data": "synthetic (random_state of acceptance.cpp:214-230, seed 0x5eed)",
+            "config": {"workload": desc, "config": a.config, "points_per_step": pts,
+                       "bytes_per_point": (n_in + n_out) * esize,
+                       "parallelism": f"reference Backend::parallel(0, {threads}) on host cores"},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "Gpoints/s", "cores": threads,
+                             "kind": "reference",
+                             "sample": f"{pts} points per step (bounded sample of the "
+                                       f"{a.n or n_default}-point workload), unmodified "
+                                       f"reference evaluate_block/evaluate with its runtime JIT"},
+            "e2e": {"value": value, "unit": "Gpoints/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
+    else:
+        line = device_run(a, rank, world, local)
+    if rank == 0:
+        text = json.dumps(line)
+        print(text, flush=True)
+        if a.out:
+            with open(a.out, "a") as f:
+                f.write(text + "\n")
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

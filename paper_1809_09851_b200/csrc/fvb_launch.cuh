@@ -1,0 +1,164 @@
+// fvb_launch.cuh -- host-side launch of the fused pointwise kernel.
+//
+// Grid policy: a grid-stride ("persistent") launch of SMs x resident CTAs per
+// SM, 256 threads per CTA, so every one of the 148 SMs stays full for the
+// whole pass and no tail wave exists; smaller problems get fewer CTAs.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+#include <string>
+
+#include "fvb.h"
+#include "fvb_stream.cuh"
+
+namespace fvb {
+
+// Per-thread error message behind fvb_last_error().
+void set_error(const std::string& msg);
+fvb_status fail(fvb_status s, const std::string& msg);
+fvb_status cuda_fail(cudaError_t e, const char* what);
+
+int device_sm_count();
+
+// Launch tuning, read once from the environment (bench sweeps only; the
+// defaults are the measured best):
+//   FVB_VEC    elements per access: 0 = 32 bytes (default), else 1/2/4/8
+//   FVB_UNROLL groups per thread per trip: 1 (default) or 2
+//   FVB_STORE  0 = st.global, 1 = st.global.cs (default), 2 = L1::no_allocate
+//   FVB_CTAS   CTAs per SM cap (0 = occupancy limit)
+struct Tuning {
+    int vec = 0;
+    int unroll = 1;
+    int store = kStoreStreaming;
+    int ctas_per_sm = 0;
+};
+const Tuning& tuning();
+
+template <class T>
+Consts<T> make_consts(const fvb_gas* g) {
+    const double gm1 = g ? g->gamma_minus_one : 2.0 / 5.0;
+    const double gamma = g ? g->gamma : 7.0 / 5.0;
+    const double cv = g ? g->cv : 5.0 / 2.0;
+    // narrow_value: constants are rounded to the computing precision first
+    // (proj/src/scalar_ops.hpp:83-85).
+    return Consts<T>{static_cast<T>(0.5), static_cast<T>(gm1), static_cast<T>(gamma),
+                     static_cast<T>(cv),  static_cast<T>(0.0), static_cast<T>(1.0)};
+}
+
+template <class Kernel>
+int resident_ctas(Kernel k) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    const int cap = tuning().ctas_per_sm;
+    return cap > 0 && cap < per_sm ? cap : per_sm;
+}
+
+// Split [0, n) into an unaligned scalar head, V-wide groups and a scalar
+// tail.  All planes must share one address residue modulo V*sizeof(T);
+// returns false when they do not (caller drops to V = 1).
+template <class T, int V>
+bool plan_range(const void* const* ptrs, int count, uint64_t n, Range* rg) {
+    const uintptr_t mod = uintptr_t(V) * sizeof(T);
+    uintptr_t res = 0;
+    for (int i = 0; i < count; ++i) {
+        const uintptr_t r = reinterpret_cast<uintptr_t>(ptrs[i]) % mod;
+        if (i == 0)
+            res = r;
+        else if (r != res)
+            return false;
+    }
+    uint64_t head = res ? (mod - res) / sizeof(T) : 0;
+    if (head > n) head = n;
+    rg->head = head;
+    rg->groups = (n - head) / V;
+    rg->tail = n - head - rg->groups * V;
+    return true;
+}
+
+template <class Op, class T, int V, int U, int SP, bool RED>
+fvb_status launch_fixed(const Planes<T, Op::NIN, Op::NOUT>& pl, const Consts<T>& k,
+                        const Range& rg, typename Bits<T>::U* red, cudaStream_t stream) {
+    auto kern = pointwise_kernel<Op, T, V, U, SP, RED>;
+    static const int per_sm = resident_ctas(kern);
+    const uint64_t threads = 256;
+    const uint64_t want = (rg.groups + threads * U - 1) / (threads * U);
+    const uint64_t cap = uint64_t(device_sm_count()) * uint64_t(per_sm);
+    uint64_t grid = want < cap ? want : cap;
+    if (grid == 0) grid = 1;
+    kern<<<unsigned(grid), unsigned(threads), 0, stream>>>(pl, k, rg, red);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? FVB_OK : cuda_fail(e, "kernel launch");
+}
+
+template <class T>
+constexpr int vec32() {
+    return int(32 / sizeof(T));
+}
+
+// Dispatch on the tuning knobs.  Only the headline kernels (TUNABLE) get the
+// full variant set; everything else runs the default configuration.
+template <class Op, class T, bool RED, bool TUNABLE>
+fvb_status launch_op(const T* const* in, T* const* out, uint64_t n, const Consts<T>& k,
+                     typename Bits<T>::U* red, cudaStream_t stream) {
+    // n == 0 is a no-op even with NULL planes (an empty torch tensor or
+    // DenseVector has no storage), as evaluate() returns early for n == 0.
+    if (n == 0) return FVB_OK;
+    Planes<T, Op::NIN, Op::NOUT> pl;
+    const void* ptrs[Op::NIN + (Op::NOUT > 0 ? Op::NOUT : 1)];
+    int np = 0;
+    for (int i = 0; i < Op::NIN; ++i) {
+        if (!in[i]) return fail(FVB_EARG, "NULL input plane");
+        if (reinterpret_cast<uintptr_t>(in[i]) % sizeof(T))
+            return fail(FVB_EALIGN, "input plane is not element-aligned");
+        pl.in[i] = in[i];
+        ptrs[np++] = in[i];
+    }
+    for (int j = 0; j < Op::NOUT; ++j) {
+        if (!out[j]) return fail(FVB_EARG, "NULL output plane");
+        if (reinterpret_cast<uintptr_t>(out[j]) % sizeof(T))
+            return fail(FVB_EALIGN, "output plane is not element-aligned");
+        pl.out[j] = out[j];
+        ptrs[np++] = out[j];
+    }
+    if (Op::NOUT == 0) pl.out[0] = nullptr;
+
+    constexpr int VD = vec32<T>();
+    const Tuning& t = tuning();
+    Range rg;
+    if (TUNABLE) {
+        const int v = t.vec ? t.vec : VD;
+        const int u = t.unroll == 2 ? 2 : 1;
+        const int sp = t.store;
+#define FVB_TRY(VV, UU, SS)                                                          \
+    if (v == VV && u == UU && sp == SS && plan_range<T, VV>(ptrs, np, n, &rg))       \
+        return launch_fixed<Op, T, VV, UU, SS, RED>(pl, k, rg, red, stream);
+#define FVB_TRY_V(VV)     \
+    FVB_TRY(VV, 1, 0)     \
+    FVB_TRY(VV, 1, 1)     \
+    FVB_TRY(VV, 1, 2)     \
+    FVB_TRY(VV, 2, 0)     \
+    FVB_TRY(VV, 2, 1)     \
+    FVB_TRY(VV, 2, 2)
+        if constexpr (sizeof(T) == 8) {
+            FVB_TRY_V(2)
+            FVB_TRY_V(4)
+        } else {
+            FVB_TRY_V(4)
+            FVB_TRY_V(8)
+        }
+#undef FVB_TRY_V
+#undef FVB_TRY
+    }
+    if (plan_range<T, VD>(ptrs, np, n, &rg))
+        return launch_fixed<Op, T, VD, 1, kStoreStreaming, RED>(pl, k, rg, red, stream);
+    // Planes with different 32-byte residues: element-wide accesses.
+    plan_range<T, 1>(ptrs, np, n, &rg);
+    return launch_fixed<Op, T, 1, 1, kStoreStreaming, RED>(pl, k, rg, red, stream);
+}
+
+}  // namespace fvb

@@ -1,0 +1,292 @@
+"""Typed wrappers over the C ABI for torch CUDA tensors.
+
+Planes are 1-D contiguous CUDA tensors (float32 or float64), one per field,
+structure-of-arrays as in the reference (a conservative state is
+``[rho, m_0..m_{d-1}, rhoE]``, proj/include/fusevec/fluid.hpp:81-88).  Every
+call enqueues on the current torch stream (or ``stream=``) and returns
+without synchronising.  Validation mirrors the reference's validate()
+(proj/src/backend_eval.cpp:236-265): plane lengths must agree
+(LengthMismatch) and precisions must be uniform (PrecisionError) before any
+kernel is enqueued.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import torch
+
+from . import _native as N
+
+
+@dataclass(frozen=True)
+class Gas:
+    """EosSpec(cp, cv) as rationals (proj/include/fusevec/fluid.hpp:27-45)."""
+
+    cp_num: int = 7
+    cp_den: int = 2
+    cv_num: int = 5
+    cv_den: int = 2
+
+    @property
+    def gamma_minus_one(self) -> float:
+        # (R/cv).value() with R = cp - cv, both exact rationals (fluid.cpp:51-53)
+        from fractions import Fraction
+        cp, cv = Fraction(self.cp_num, self.cp_den), Fraction(self.cv_num, self.cv_den)
+        r = (cp - cv) / cv
+        return float(r.numerator) / float(r.denominator)
+
+    @property
+    def gamma(self) -> float:
+        from fractions import Fraction
+        g = Fraction(self.cp_num, self.cp_den) / Fraction(self.cv_num, self.cv_den)
+        return float(g.numerator) / float(g.denominator)
+
+    @property
+    def cv(self) -> float:
+        from fractions import Fraction
+        c = Fraction(self.cv_num, self.cv_den)
+        return float(c.numerator) / float(c.denominator)
+
+    def struct(self) -> N.GasStruct:
+        return N.GasStruct(self.gamma_minus_one, self.gamma, self.cv)
+
+
+DEFAULT_GAS = Gas()
+
+_PREC = {torch.float32: 0, torch.float64: 1}
+_DTYPE = {0: torch.float32, 1: torch.float64}
+
+
+def _gas_ptr(gas: Optional[Gas]):
+    if gas is None:
+        return None
+    return ctypes.byref(gas.struct())
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def _planes(planes: Sequence[torch.Tensor], what: str, n: Optional[int] = None,
+            prec: Optional[int] = None):
+    ptrs = []
+    for t in planes:
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise N.ArgumentError(N.FVB_EARG, f"{what}: planes must be CUDA tensors")
+        if t.dim() != 1 or not t.is_contiguous():
+            raise N.ArgumentError(N.FVB_EARG, f"{what}: planes must be contiguous 1-D")
+        p = _PREC.get(t.dtype)
+        if p is None:
+            raise N.PrecisionError(N.FVB_EPREC, f"{what}: dtype {t.dtype} is not f32/f64")
+        if prec is None:
+            prec = p
+        elif p != prec:
+            raise N.PrecisionError(N.FVB_EPREC, f"{what}: mixed precisions")
+        if n is None:
+            n = t.numel()
+        elif t.numel() != n:
+            raise N.LengthMismatch(N.FVB_ELEN,
+                                   f"{what}: plane length {t.numel()} does not match {n}")
+        ptrs.append(t.data_ptr())
+    return ptrs, n, prec
+
+
+def _alloc(count: int, n: int, prec: int, device) -> list:
+    return [torch.empty(n, dtype=_DTYPE[prec], device=device) for _ in range(count)]
+
+
+def _state(state, dim):
+    if len(state) != dim + 2:
+        raise N.ArgumentError(N.FVB_EARG, f"a {dim}D state needs {dim + 2} planes, "
+                                          f"got {len(state)}")
+    return _planes(state, "state")
+
+
+def flux(state: Sequence[torch.Tensor], dim: int, out=None, gas: Optional[Gas] = None,
+         stream=None):
+    """inviscid_flux of a conservative state: (d+2)*d planes, item r*d+c."""
+    ins, n, prec = _state(state, dim)
+    if out is None:
+        out = _alloc((dim + 2) * dim, n, prec, state[0].device)
+    outs, _, _ = _planes(out, "flux out", n, prec)
+    N.check(N.lib().fvb_flux(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins), N.ptr_array(outs),
+                             _stream(stream)))
+    return out
+
+
+def cons2prim(state, dim, out=None, gas=None, stream=None):
+    """[v_0..v_{d-1}, p, c] of a conservative state."""
+    ins, n, prec = _state(state, dim)
+    if out is None:
+        out = _alloc(dim + 2, n, prec, state[0].device)
+    outs, _, _ = _planes(out, "cons2prim out", n, prec)
+    N.check(N.lib().fvb_cons2prim(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins),
+                                  N.ptr_array(outs), _stream(stream)))
+    return out
+
+
+def prim2cons(prim, dim, out=None, gas=None, stream=None):
+    """[m_0..m_{d-1}, rhoE] of a primitive state [rho, v.., p]."""
+    ins, n, prec = _state(prim, dim)
+    if out is None:
+        out = _alloc(dim + 1, n, prec, prim[0].device)
+    outs, _, _ = _planes(out, "prim2cons out", n, prec)
+    N.check(N.lib().fvb_prim2cons(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins),
+                                  N.ptr_array(outs), _stream(stream)))
+    return out
+
+
+def v_mag2(state, dim, out=None, stream=None):
+    ins, n, prec = _state(state, dim)
+    if out is None:
+        out = _alloc(1, n, prec, state[0].device)[0]
+    outs, _, _ = _planes([out], "v_mag2 out", n, prec)
+    N.check(N.lib().fvb_v_mag2(dim, prec, n, N.ptr_array(ins), outs[0], _stream(stream)))
+    return out
+
+
+def eos(rho, e, p=None, T=None, gas=None, stream=None):
+    """Ideal-gas closures: returns (p, T)."""
+    ins, n, prec = _planes([rho, e], "eos")
+    if p is None:
+        p = _alloc(1, n, prec, rho.device)[0]
+    if T is None:
+        T = _alloc(1, n, prec, rho.device)[0]
+    outs, _, _ = _planes([p, T], "eos out", n, prec)
+    N.check(N.lib().fvb_eos(_gas_ptr(gas), prec, n, ins[0], ins[1], outs[0], outs[1],
+                            _stream(stream)))
+    return p, T
+
+
+def jacobian(state, dim, out=None, lambda_max=True, gas=None, stream=None):
+    """Flux Jacobians [k][r][c] (d*(d+2)^2 planes) and, unless lambda_max is
+    False, a 0-d device tensor holding the CFL max wave speed."""
+    ins, n, prec = _state(state, dim)
+    w = dim + 2
+    if out is None:
+        out = _alloc(dim * w * w, n, prec, state[0].device)
+    outs, _, _ = _planes(out, "jacobian out", n, prec)
+    lam = None
+    if lambda_max is True:
+        lam = torch.empty((), dtype=_DTYPE[prec], device=state[0].device)
+    elif isinstance(lambda_max, torch.Tensor):
+        lam = lambda_max
+    N.check(N.lib().fvb_jacobian(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins),
+                                 N.ptr_array(outs), lam.data_ptr() if lam is not None else None,
+                                 _stream(stream)))
+    return out, lam
+
+
+def wave_speed_max(state, dim, lam_out=None, lambda_max=None, gas=None, stream=None):
+    """CFL reduction: returns (lambda per point or None, 0-d lambda_max)."""
+    ins, n, prec = _state(state, dim)
+    if lambda_max is None:
+        lambda_max = torch.empty((), dtype=_DTYPE[prec], device=state[0].device)
+    lp = None
+    if lam_out is not None:
+        lp = _planes([lam_out], "lambda out", n, prec)[0][0]
+    N.check(N.lib().fvb_wave_speed_max(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins), lp,
+                                       lambda_max.data_ptr(), _stream(stream)))
+    return lam_out, lambda_max
+
+
+def axpy_sin(x, y, stream=None):
+    """y <- 0.5*sin(x+y) in place."""
+    ptrs, n, prec = _planes([x, y], "axpy_sin")
+    N.check(N.lib().fvb_axpy_sin(prec, n, ptrs[0], ptrs[1], _stream(stream)))
+    return y
+
+
+def synth_state(dim, n, prec=1, seed=0x5EED, first=0, out=None, device="cuda", stream=None):
+    """random_state of acceptance.cpp:214-230 for global points [first, first+n)."""
+    if out is None:
+        out = _alloc(dim + 2, n, prec, device)
+    outs, _, p = _planes(out, "synth out", n, None) if n else ([0] * (dim + 2), 0, prec)
+    N.check(N.lib().fvb_synth_state(dim, prec, seed, first, n, N.ptr_array(outs),
+                                    _stream(stream)))
+    return out
+
+
+def synth_uniform(n, prec=1, seed=1, first=0, lo=0.25, hi=4.0, out=None, device="cuda",
+                  stream=None):
+    """make_vec of oracle.hpp:118-123: uniform(lo, hi) of draws [first, first+n)."""
+    if out is None:
+        out = _alloc(1, n, prec, device)[0]
+    ptr = out.data_ptr() if n else None
+    N.check(N.lib().fvb_synth_uniform(prec, seed, first, n, lo, hi, ptr, _stream(stream)))
+    return out
+
+
+def patterns():
+    """[(name, pattern key)] of every registered fused kernel."""
+    L = N.lib()
+    out = []
+    for i in range(L.fvb_pattern_count()):
+        name = ctypes.c_char_p()
+        text = L.fvb_pattern(i, ctypes.byref(name))
+        out.append((name.value.decode(), text.decode()))
+    return out
+
+
+def lookup(key: str) -> N.KernelStruct:
+    """fvb_lookup: the fused kernel for a structural key (raises
+    UnsupportedExpression when none exists)."""
+    k = N.KernelStruct()
+    N.check(N.lib().fvb_lookup(key.encode(), ctypes.byref(k)))
+    return k
+
+
+class HostContext:
+    """fvb_ctx: the host-buffer (end-to-end) path over pinned/pageable memory."""
+
+    def __init__(self, device: int = 0, chunk_points: int = 0):
+        self._h = ctypes.c_void_p()
+        N.check(N.lib().fvb_ctx_create(device, chunk_points, ctypes.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            N.lib().fvb_ctx_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _host(planes, what, n=None, prec=None):
+        ptrs = []
+        for t in planes:
+            if t.is_cuda or t.dim() != 1 or not t.is_contiguous():
+                raise N.ArgumentError(N.FVB_EARG, f"{what}: host planes must be CPU 1-D")
+            p = _PREC[t.dtype]
+            prec = p if prec is None else prec
+            if p != prec:
+                raise N.PrecisionError(N.FVB_EPREC, f"{what}: mixed precisions")
+            n = t.numel() if n is None else n
+            if t.numel() != n:
+                raise N.LengthMismatch(N.FVB_ELEN, f"{what}: ragged planes")
+            ptrs.append(t.data_ptr())
+        return ptrs, n, prec
+
+    def flux(self, state, dim, out, gas=None):
+        ins, n, prec = self._host(state, "state")
+        outs, _, _ = self._host(out, "out", n, prec)
+        N.check(N.lib().fvb_flux_host(self._h, _gas_ptr(gas), dim, prec, n, N.ptr_array(ins),
+                                      N.ptr_array(outs)))
+        return out
+
+    def jacobian(self, state, dim, out, gas=None):
+        ins, n, prec = self._host(state, "state")
+        outs, _, _ = self._host(out, "out", n, prec)
+        lam = ctypes.c_double()
+        N.check(N.lib().fvb_jacobian_host(self._h, _gas_ptr(gas), dim, prec, n,
+                                          N.ptr_array(ins), N.ptr_array(outs),
+                                          ctypes.byref(lam)))
+        return out, lam.value

@@ -1,0 +1,40 @@
+"""Shared fixtures.  `-m gpu` tests need a CUDA device and the built
+libfvb.so; they fail (never skip into a fallback) when either is missing."""
+
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (runs under gpurun / the driver)")
+    config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+@pytest.fixture(scope="session")
+def orc():
+    import oracle
+    return oracle.oracle()
+
+
+@pytest.fixture(scope="session")
+def ref():
+    import oracle
+    r = oracle.reference()
+    if r is None:
+        pytest.skip("reference build oracle/_ref/libfvref.so not present")
+    return r
+
+
+@pytest.fixture(scope="session")
+def cuda():
+    import torch
+    assert torch.cuda.is_available(), "gpu-marked test run without a CUDA device"
+    import paper_1809_09851_b200 as fvb
+    fvb.lib()  # raises if libfvb.so is missing: no fallback path exists
+    return torch.device("cuda:0")

@@ -1,0 +1,158 @@
+"""The C-ABI library on CPU: it loads, exports every symbol include/fvb.h
+declares, validates arguments before touching the device, and resolves
+structural keys (host-only code, no GPU needed)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_1809_09851_b200 as fvb
+from paper_1809_09851_b200 import _native as N
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    text = open(os.path.join(ROOT, "include", "fvb.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    names = set(re.findall(r"\b(fvb_[a-z0-9_]+)\s*\(", text))
+    return sorted(n for n in names if n not in ("fvb_kernel_fn", "fvb_status"))
+
+
+def test_library_loads_and_reports():
+    L = fvb.lib()
+    assert L.fvb_abi_version() == 1
+    info = L.fvb_build_info().decode()
+    assert "sm_100a" in info and "fmad=false" in info
+
+
+def test_exports_every_declared_symbol():
+    declared = header_functions()
+    assert len(declared) >= 18
+    out = subprocess.run(["nm", "-D", "--defined-only", fvb.lib_path()], check=True,
+                         capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (fvb_\w+)", out))
+    missing = [n for n in declared if n not in exported]
+    assert not missing, missing
+    # the binding declares exactly the header's entry points
+    assert sorted(N.EXPORTED) == declared
+    # and nothing from the C++ internals leaks (hidden visibility)
+    assert all(n.startswith("fvb_") for n in exported)
+
+
+def test_sm100a_sass_present():
+    out = subprocess.run(["cuobjdump", "--list-elf", fvb.lib_path()], capture_output=True,
+                         text=True)
+    assert "sm_100a" in out.stdout
+
+
+@pytest.mark.parametrize("dim,prec,status", [(0, 1, N.FVB_EARG), (4, 1, N.FVB_EARG),
+                                             (3, 2, N.FVB_EPREC)])
+def test_argument_validation_before_launch(dim, prec, status):
+    L = fvb.lib()
+    arr = N.ptr_array([0] * 20)
+    assert L.fvb_flux(None, dim, prec, 10, arr, arr, None) == status
+    assert L.fvb_last_error().decode()
+
+
+def test_zero_length_is_noop():
+    L = fvb.lib()
+    arr = N.ptr_array([0] * 80)
+    for d in (1, 2, 3):
+        for p in (0, 1):
+            assert L.fvb_flux(None, d, p, 0, arr, arr, None) == N.FVB_OK
+            assert L.fvb_cons2prim(None, d, p, 0, arr, arr, None) == N.FVB_OK
+            assert L.fvb_jacobian(None, d, p, 0, arr, arr, None, None) == N.FVB_OK
+
+
+def test_bad_gas_rejected():
+    L = fvb.lib()
+    arr = N.ptr_array([0] * 20)
+    bad = N.GasStruct(0.0, 1.0, 2.5)
+    assert L.fvb_flux(ctypes.byref(bad), 3, 1, 10, arr, arr, None) == N.FVB_EARG
+
+
+def test_errors_map_to_reference_names():
+    with pytest.raises(fvb.PrecisionError):
+        N.check(N.FVB_EPREC)
+    with pytest.raises(fvb.UnsupportedExpression):
+        fvb.lookup("dB9d(Ld0;,Ld1;)")
+
+
+def test_patterns_cover_every_block():
+    names = {n for n, _ in fvb.patterns()}
+    for d in (1, 2, 3):
+        for p in ("f32", "f64"):
+            for block in ("flux", "cons2prim", "cons2prim_c", "prim2cons", "jacobian",
+                          "pressure", "sound_speed", "v_mag2", "wave_speed"):
+                assert f"{block}{d}_{p}" in names
+    for p in ("f32", "f64"):
+        assert {f"axpy_sin_{p}", f"eos_p_{p}", f"eos_T_{p}"} <= names
+
+
+def hexbits(x):
+    import struct
+    return "%016x" % struct.unpack("<Q", struct.pack("<d", x))[0]
+
+
+def axpy_key(c=0.5):
+    # key_node of constant(0.5, leaf(y)) * elem_sin(leaf(x) + leaf(y)) with
+    # dest precision f64 (proj/src/backend_jit.cpp:112-155, 319-322)
+    return f"dB2d(Cd{hexbits(c)};,U2d(B0d(Ld0;,Ld1;)))"
+
+
+def test_lookup_axpy_key_captures_constant():
+    k = fvb.lookup(axpy_key())
+    assert k.name.decode() == "axpy_sin_f64"
+    assert (k.n_outputs, k.n_inputs, k.prec) == (1, 2, 1)
+    assert k.consts[0] == 0.5
+    assert list(k.in_slot[:2]) == [0, 1]
+    k2 = fvb.lookup(axpy_key(0.25))
+    assert k2.consts[0] == 0.25
+
+
+def test_lookup_rejects_near_misses():
+    for bad in [axpy_key()[:-1], axpy_key() + ")", axpy_key().replace("U2d", "U3d"),
+                axpy_key().replace("Ld1;", "Ld0;"), "s" + axpy_key()[1:]]:
+        with pytest.raises(fvb.UnsupportedExpression):
+            fvb.lookup(bad)
+
+
+def test_every_pattern_resolves_with_default_constants():
+    defaults = {"half": 0.5, "gm1": 0.4, "gamma": 1.4, "cv": 2.5, "zero": 0.0, "one": 1.0}
+    import struct
+    for name, pat in fvb.patterns():
+        f32 = name.endswith("_f32")
+
+        def sub(m):
+            v = defaults[m.group(2)]
+            if f32:
+                v = struct.unpack("<f", struct.pack("<f", v))[0]
+            return f"C{m.group(1)}{hexbits(v)};"
+
+        key = re.sub(r"C([sd])#(\w+);", sub, pat)
+        k = fvb.lookup(key)
+        assert k.name.decode() == name
+        assert all(s >= 0 for s in k.in_slot[:k.n_inputs])
+
+
+def test_inconsistent_named_constant_rejected():
+    # the two occurrences of gm1 in one flux block must carry the same bits
+    pat = dict(fvb.patterns())["flux1_f64"]
+    first = [True]
+
+    def sub(m):
+        name = m.group(2)
+        v = {"half": 0.5, "gm1": 0.4}[name]
+        if name == "gm1" and not first[0]:
+            v = 0.5
+        if name == "gm1":
+            first[0] = False
+        return f"Cd{hexbits(v)};"
+
+    key = re.sub(r"C([sd])#(\w+);", sub, pat)
+    with pytest.raises(fvb.UnsupportedExpression):
+        fvb.lookup(key)

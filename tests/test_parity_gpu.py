@@ -1,0 +1,377 @@
+"""Device parity: every kernel of libfvb.so against the CPU oracle (which
+tests/test_oracle.py pins to the reference bit for bit).
+
+Bars (BASELINE.json north_star): bitwise for +,-,*,/,sqrt (the whole fluid
+path: flux, cons->prim, EOS, Jacobians, wave speed) and for the synthetic
+generators; the CFL maximum exactly; sin within 4 ulp (f64) / rel 1e-6
+(f32).  Runs only on a B200 (`-m gpu`), through the C ABI.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1809_09851_b200 as fvb
+from paper_1809_09851_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+DT = {"f64": torch.float64, "f32": torch.float32}
+NP = {"f64": np.float64, "f32": np.float32}
+PREC = {"f32": 0, "f64": 1}
+SIZES = [0, 1, 2, 3, 5, 7, 8, 31, 1023, 1025, 4099, 65537]
+
+
+def to_dev(arrs, dev):
+    return [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in arrs]
+
+
+def to_host(ts):
+    torch.cuda.synchronize()
+    return [t.cpu().numpy() for t in ts]
+
+
+def same_bits(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return a.dtype == b.dtype and a.shape == b.shape and a.tobytes() == b.tobytes()
+
+
+def all_same(xs, ys):
+    return len(xs) == len(ys) and all(same_bits(x, y) for x, y in zip(xs, ys))
+
+
+def ulp_diff(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    ia = a.view(np.int64)
+    ib = b.view(np.int64)
+    ia = np.where(ia < 0, np.int64(-0x8000000000000000) - ia, ia)
+    ib = np.where(ib < 0, np.int64(-0x8000000000000000) - ib, ib)
+    return np.abs(ia - ib)
+
+
+# ---- synthetic inputs ---------------------------------------------------------
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("dim", [1, 2, 3])
+def test_synth_state_bitwise(cuda, orc, prec, dim):
+    for n, first in [(1, 0), (1000, 0), (4099, 123456789)]:
+        dev = fvb.synth_state(dim, n, prec=PREC[prec], seed=0x5EED, first=first)
+        want = orc.random_state(dim, n, seed=0x5EED, first=first, prec=prec)
+        assert all_same(to_host(dev), want)
+
+
+def test_synth_uniform_bitwise(cuda, orc):
+    for prec in ("f64", "f32"):
+        d = fvb.synth_uniform(3000, prec=PREC[prec], seed=1, first=3000)
+        assert same_bits(to_host([d])[0], orc.make_vec(1, 3000, 3000, prec=prec))
+
+
+# ---- fluid blocks, bitwise ----------------------------------------------------------
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("dim", [1, 2, 3])
+def test_fluid_blocks_bitwise(cuda, orc, prec, dim):
+    for n in SIZES:
+        s_np = orc.random_state(dim, n, seed=0xF1 + n, prec=prec)
+        s = to_dev(s_np, cuda)
+        assert all_same(to_host(fvb.flux(s, dim)), orc.flux(dim, s_np)), ("flux", n)
+        c = to_host(fvb.cons2prim(s, dim))
+        assert all_same(c, orc.cons2prim(dim, s_np)), ("cons2prim", n)
+        prim_np = [s_np[0]] + c[:dim] + [c[dim]]
+        assert all_same(to_host(fvb.prim2cons(to_dev(prim_np, cuda), dim)),
+                        orc.prim2cons(dim, prim_np)), ("prim2cons", n)
+        assert same_bits(to_host([fvb.v_mag2(s, dim)])[0], orc.v_mag2(dim, s_np))
+        j, lam = fvb.jacobian(s, dim)
+        j_np, lam_np = orc.jacobian(dim, s_np)
+        assert all_same(to_host(j), j_np), ("jacobian", n)
+        assert same_bits(lam.cpu().numpy(), np.asarray(lam_np)), ("lambda", n)
+        _, lam2 = fvb.wave_speed_max(s, dim)
+        assert same_bits(lam2.cpu().numpy(), np.asarray(lam_np))
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("dim", [1, 2, 3])
+def test_golden_fixtures(cuda, prec, dim):
+    z = np.load(os.path.join(GOLDEN, f"fluid_{prec}_d{dim}.npz"))
+    s = to_dev(list(z["state"]), cuda)
+    assert same_bits(np.stack(to_host(fvb.flux(s, dim))), z["flux"])
+    assert same_bits(np.stack(to_host(fvb.cons2prim(s, dim))), z["cons2prim"])
+    assert same_bits(np.stack(to_host(fvb.prim2cons(to_dev(list(z["prim"]), cuda), dim))),
+                     z["prim2cons"])
+    assert same_bits(to_host([fvb.v_mag2(s, dim)])[0], z["v_mag2"])
+    j, lam = fvb.jacobian(s, dim)
+    assert same_bits(np.stack(to_host(j)), z["jacobian"])
+    assert float(lam.item()) == float(z["lambda_max"])
+    lam_pts = torch.empty_like(s[0])
+    fvb.wave_speed_max(s, dim, lam_out=lam_pts)
+    assert same_bits(to_host([lam_pts])[0], z["wave_speed"])
+
+
+def test_golden_eos_and_monatomic(cuda):
+    z = np.load(os.path.join(GOLDEN, "eos.npz"))
+    p, T = fvb.eos(*to_dev([z["rho"], z["e"]], cuda))
+    assert same_bits(p.cpu().numpy(), z["p"]) and same_bits(T.cpu().numpy(), z["T"])
+    mono = fvb.Gas(5, 2, 3, 2)
+    p, T = fvb.eos(*to_dev([z["rho"], z["e"]], cuda), gas=mono)
+    assert same_bits(p.cpu().numpy(), z["p_mono"]) and same_bits(T.cpu().numpy(), z["T_mono"])
+    c = fvb.cons2prim(to_dev(list(z["mono_state"]), cuda), 1, gas=mono)
+    assert same_bits(np.stack(to_host(c)), z["mono_cons2prim"])
+    assert c[1].item() == 2.0  # test_fluid.cpp:347-353
+
+
+def test_gas_variant_bitwise(cuda, orc):
+    g = fvb.Gas(5, 2, 3, 2)
+    og = orc.gas(cp=(5, 2), cv=(3, 2))
+    s_np = orc.random_state(3, 5000, seed=3)
+    s = to_dev(s_np, cuda)
+    assert all_same(to_host(fvb.flux(s, 3, gas=g)), orc.flux(3, s_np, gas=og))
+    j, lam = fvb.jacobian(s, 3, gas=g)
+    j_np, lam_np = orc.jacobian(3, s_np, gas=og)
+    assert all_same(to_host(j), j_np) and lam.item() == lam_np
+
+
+# ---- known answers on the device ----------------------------------------------
+
+
+def test_worked_instance(cuda):
+    s = [torch.tensor([v], dtype=torch.float64, device=cuda) for v in (2.0, 2.0, 4.0, 4.0, 14.0)]
+    f = [t.item() for t in fvb.flux(s, 3)]
+    assert [f[r * 3] for r in range(5)] == [2.0, 4.0, 4.0, 4.0, 16.0]
+    c = [t.item() for t in fvb.cons2prim(s, 3)]
+    assert c[:4] == [1.0, 2.0, 2.0, 2.0] and c[4] == 1.1832159566199232
+    j, lam = fvb.jacobian(s, 3)
+    A0 = np.array([t.item() for t in j[:25]]).reshape(5, 5)
+    assert np.allclose(A0, [[0, 1, 0, 0, 0], [0.8, 1.6, -0.8, -0.8, 0.4], [-2, 2, 1, 0, 0],
+                            [-2, 2, 0, 1, 0], [-6.2, 7.6, -0.8, -0.8, 1.4]], rtol=0, atol=1e-15)
+    assert lam.item() == 4.183215956619923
+
+
+# ---- layout edge cases ----------------------------------------------------------
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_unaligned_and_mixed_residue_planes(cuda, orc, prec):
+    # Slices at element offsets exercise the scalar head/tail, and planes with
+    # different 32-byte residues the element-wide fallback.
+    dim, n = 3, 5003
+    s_np = orc.random_state(dim, n, seed=77, prec=prec)
+    want = orc.flux(dim, s_np)
+    for offsets in [(1,) * 5, (3,) * 5, (0, 1, 2, 3, 1)]:
+        s = []
+        for a, off in zip(s_np, offsets):
+            buf = torch.empty(n + 8, dtype=DT[prec], device=cuda)
+            buf[off:off + n] = torch.from_numpy(a).to(cuda)
+            s.append(buf[off:off + n])
+        outs = []
+        for j in range(15):
+            buf = torch.empty(n + 8, dtype=DT[prec], device=cuda)
+            off = offsets[j % 5]
+            outs.append(buf[off:off + n])
+        fvb.flux(s, dim, out=outs)
+        assert all_same(to_host(outs), want), offsets
+
+
+def test_validation_errors(cuda):
+    a = torch.zeros(10, dtype=torch.float64, device=cuda)
+    b = torch.zeros(11, dtype=torch.float64, device=cuda)
+    c = torch.zeros(10, dtype=torch.float32, device=cuda)
+    with pytest.raises(fvb.LengthMismatch):
+        fvb.flux([a, a, a, a, b], 3)
+    with pytest.raises(fvb.PrecisionError):
+        fvb.flux([a, a, a, a, c], 3)
+    with pytest.raises(fvb.ArgumentError):
+        fvb.flux([a, a, a], 3)
+
+
+# ---- CFL maximum ------------------------------------------------------------------
+
+
+def test_lambda_max_exact_and_nan(cuda, orc):
+    dim, n = 3, 2_000_003
+    s_np = orc.random_state(dim, n, seed=5)
+    s = to_dev(s_np, cuda)
+    _, lam = fvb.wave_speed_max(s, dim)
+    assert lam.item() == orc.wave_speed_max(dim, s_np)
+    # NaN anywhere propagates (CFL max definition)
+    s[0][n // 2] = float("nan")
+    _, lam = fvb.wave_speed_max(s, dim)
+    assert np.isnan(lam.item())
+    # empty range -> 0
+    e = [torch.empty(0, dtype=torch.float64, device=cuda) for _ in range(5)]
+    _, lam = fvb.wave_speed_max(e, dim)
+    assert lam.item() == 0.0
+
+
+def test_lambda_invariant_to_slicing(cuda, orc):
+    # Shard the range like the multi-GPU path; the max over slice maxima is
+    # bitwise the global max (order-independent reduction).
+    dim, n = 3, 1_000_001
+    s = fvb.synth_state(dim, n, seed=0x5EED)
+    _, whole = fvb.wave_speed_max(s, dim)
+    for G in (2, 3, 8):
+        parts = []
+        for g in range(G):
+            lo, hi = g * n // G, (g + 1) * n // G
+            _, m = fvb.wave_speed_max([t[lo:hi] for t in s], dim)
+            parts.append(m.item())
+        assert max(parts) == whole.item()
+
+
+# ---- axpy-sin: sin within 4 ulp --------------------------------------------------
+
+
+def test_axpy_sin(cuda, orc):
+    z = np.load(os.path.join(GOLDEN, "axpy_sin.npz"))
+    x, y = to_dev([z["x"], z["y"]], cuda)
+    fvb.axpy_sin(x, y)  # in place, dest aliases a leaf
+    got = y.cpu().numpy()
+    assert ulp_diff(got, z["y_out"]).max() <= 4
+    x32, y32 = to_dev([z["x32"], z["y32"]], cuda)
+    fvb.axpy_sin(x32, y32)
+    got32 = y32.cpu().numpy().astype(np.float64)
+    want32 = z["y32_out"].astype(np.float64)
+    assert np.all(np.abs(got32 - want32) <= 1e-6 * np.maximum(np.abs(want32), 1.0))
+    # Figure 2: x=0, y=pi/2 -> 0.5
+    x = torch.zeros(1, dtype=torch.float64, device=cuda)
+    y = torch.full((1,), np.pi / 2, dtype=torch.float64, device=cuda)
+    assert abs(fvb.axpy_sin(x, y).item() - 0.5) <= 1e-15
+
+
+def test_axpy_sin_config1(cuda, orc):
+    # C1 at full size: N = 1e6 from the device generator, against the oracle
+    n = 1_000_000
+    x = fvb.synth_uniform(n, seed=1, first=0)
+    y = fvb.synth_uniform(n, seed=1, first=n)
+    want = orc.axpy_sin(orc.make_vec(1, 0, n), orc.make_vec(1, n, n))
+    fvb.axpy_sin(x, y)
+    assert ulp_diff(y.cpu().numpy(), want).max() <= 4
+
+
+# ---- full-size properties (BASELINE configs) ----------------------------------------
+
+
+def test_flux_1e8_sampled_bitwise(cuda, orc):
+    # C3 at N = 1e8 (16 GB of planes): every sampled point equals the oracle
+    # evaluated on the same global point (random-access generator).
+    dim, n = 3, 100_000_000
+    s = fvb.synth_state(dim, n, seed=0x5EED)
+    f = fvb.flux(s, dim)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0)
+    idx = np.unique(np.concatenate([rng.integers(0, n, 2000), [0, 1, n - 2, n - 1]]))
+    it = torch.from_numpy(idx).to(cuda)
+    got = np.stack([t[it].cpu().numpy() for t in f])
+    for k, i in enumerate(idx):
+        pt = orc.random_state(dim, 1, seed=0x5EED, first=int(i))
+        want = np.array([a[0] for a in orc.flux(dim, pt)])
+        assert same_bits(got[:, k], want), int(i)
+    # row 0 is the momentum planes bit for bit
+    for j in range(3):
+        assert torch.equal(f[j].view(torch.int64), s[1 + j].view(torch.int64))
+    del f, s
+    torch.cuda.empty_cache()
+
+
+def test_jacobian_cfl_1e8(cuda, orc):
+    # C4 at N = 1e8 (f32: 32 GB of outputs): sampled bitwise, fused lambda_max
+    # equals the standalone reduction and the max of per-point lambda.
+    dim, n = 3, 100_000_000
+    s = fvb.synth_state(dim, n, prec=0, seed=0x5EED)
+    j, lam = fvb.jacobian(s, dim)
+    lam_pts = torch.empty_like(s[0])
+    _, lam2 = fvb.wave_speed_max(s, dim, lam_out=lam_pts)
+    torch.cuda.synchronize()
+    assert lam.item() == lam2.item() == lam_pts.max().item()
+    rng = np.random.default_rng(1)
+    idx = rng.integers(0, n, 300)
+    it = torch.from_numpy(idx).to(cuda)
+    got = np.stack([t[it].cpu().numpy() for t in j])
+    for k, i in enumerate(idx):
+        pt = orc.random_state(dim, 1, seed=0x5EED, first=int(i), prec="f32")
+        want = np.array([a[0] for a in orc.jacobian(dim, pt)[0]], np.float32)
+        assert same_bits(got[:, k], want), int(i)
+    del j, s, lam_pts
+    torch.cuda.empty_cache()
+
+
+# ---- the host-buffer (end-to-end) path -----------------------------------------------
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_path_matches_device(cuda, orc, pinned):
+    dim, n = 3, 3_000_017
+    s_np = orc.random_state(dim, n, seed=11)
+    want = orc.flux(dim, s_np)
+    ctx = fvb.HostContext(0, chunk_points=1 << 20)
+    hs = [torch.from_numpy(a) for a in s_np]
+    outs = [torch.empty(n, dtype=torch.float64) for _ in range(15)]
+    if pinned:
+        hs = [t.pin_memory() for t in hs]
+        outs = [t.pin_memory() for t in outs]
+    ctx.flux(hs, dim, outs)
+    assert all_same([t.numpy() for t in outs], want)
+    jo = [torch.empty(n, dtype=torch.float64) for _ in range(75)]
+    _, lam = ctx.jacobian(hs, dim, jo)
+    j_np, lam_np = orc.jacobian(dim, s_np)
+    assert lam == lam_np
+    assert all_same([t.numpy() for t in jo[:25]], j_np[:25])
+    ctx.close()
+
+
+# ---- structural-key kernels -----------------------------------------------------------
+
+
+def test_lookup_kernel_launch(cuda, orc):
+    import re
+    import struct
+
+    def hexbits(v):
+        return "%016x" % struct.unpack("<Q", struct.pack("<d", v))[0]
+
+    pat = dict(fvb.patterns())["flux3_f64"]
+    key = re.sub(r"Cd#(\w+);", lambda m: "Cd" + hexbits({"half": 0.5, "gm1": 0.4}[m.group(1)])
+                 + ";", pat)
+    k = fvb.lookup(key)
+    n = 10_007
+    s_np = orc.random_state(3, n, seed=21)
+    s = to_dev(s_np, cuda)
+    names = ["rho", "m0", "m1", "m2", "E"]
+    # argument block: 15 outputs, then leaves in the key's slot order
+    slots = [None] * k.n_inputs
+    for ci in range(5):
+        slots[k.in_slot[ci]] = s[ci]
+    outs = [torch.empty(n, dtype=torch.float64, device=cuda) for _ in range(15)]
+    args = N.ptr_array([t.data_ptr() for t in outs + slots])
+    # two halves through [begin, end), like JitKernel::Fn ranges
+    stream = torch.cuda.current_stream().cuda_stream
+    for b, e in ((0, 5000), (5000, n)):
+        N.check(k.fn(ctypes.byref(k), b, e, args, stream))
+    assert all_same(to_host(outs), orc.flux(3, s_np))
+    assert names  # canonical order documented in fvb_registry.cu
+
+
+def test_cuda_graph_capture(cuda, orc):
+    dim, n = 3, 100_000
+    s = fvb.synth_state(dim, n, seed=9)
+    out = [torch.empty(n, dtype=torch.float64, device=cuda) for _ in range(15)]
+    g = torch.cuda.CUDAGraph()
+    stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(stream):
+        fvb.flux(s, dim, out=out)  # warm (occupancy query) outside capture
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=stream):
+            fvb.flux(s, dim, out=out)
+    for t in out:
+        t.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    want = orc.flux(dim, [t.cpu().numpy() for t in s])
+    assert all_same(to_host(out), want)
