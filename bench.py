@@ -87,13 +87,15 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def profiled_traffic(config, prec):
-    """DRAM bytes per launch from the committed ncu capture, or None."""
+def profiled_traffic(config, prec, n):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
+    from the committed `ncu --set full` capture of this kernel, scaled from
+    the captured launch's points to n; None when no capture is committed."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
-            t = json.load(f)
-        return t.get(f"{config}_{prec}")
+            t = json.load(f)[f"{config}_{prec}"]
+        return t["dram_bytes"] / t["points"] * n
     except Exception:
         return None
 
@@ -354,7 +356,7 @@ def device_run(a, rank, world, local):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_src,
                      "frac_of_nominal_8000": achieved / 8000.0,
-                     "traffic": profiled_traffic(a.config, a.prec),
+                     "traffic": profiled_traffic(a.config, a.prec, n),
                      "kernel_ms": kern_avg},
         "cpu_baseline": cpu,
         "e2e": e2e,

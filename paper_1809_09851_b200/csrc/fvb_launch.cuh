@@ -25,15 +25,20 @@ int device_sm_count();
 
 // Launch tuning, read once from the environment (bench sweeps only; the
 // defaults are the measured best):
-//   FVB_VEC    elements per access: 0 = 32 bytes (default), else 1/2/4/8
-//   FVB_UNROLL groups per thread per trip: 1 (default) or 2
-//   FVB_STORE  0 = st.global, 1 = st.global.cs (default), 2 = L1::no_allocate
-//   FVB_CTAS   CTAs per SM cap (0 = occupancy limit)
+//   FVB_VEC      elements per access: 32 bytes (default) or half of that
+//   FVB_UNROLL   groups per thread per trip: 1 (default) or 2
+//   FVB_THREADS  threads per CTA: 128, 256 (default) or 512
+//   FVB_MINB     __launch_bounds__ min blocks per SM: 1 (default), 2 or 4
+//   FVB_CTAS     CTAs per SM cap (0 = occupancy limit)
+// (Store policy is fixed at st.global.cs: the sweep of round 1 measured
+// st.global / .cs / L1::no_allocate within 0.1% of each other.)
 struct Tuning {
     int vec = 0;
-    int unroll = 1;
-    int store = kStoreStreaming;
+    int unroll = 0;
+    int threads = 0;
+    int min_blocks = 0;
     int ctas_per_sm = 0;
+    bool any() const { return vec || unroll || threads || min_blocks; }
 };
 const Tuning& tuning();
 
@@ -49,9 +54,9 @@ Consts<T> make_consts(const fvb_gas* g) {
 }
 
 template <class Kernel>
-int resident_ctas(Kernel k) {
+int resident_ctas(Kernel k, int threads) {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, 0) != cudaSuccess ||
         per_sm < 1)
         per_sm = 1;
     const int cap = tuning().ctas_per_sm;
@@ -80,12 +85,12 @@ bool plan_range(const void* const* ptrs, int count, uint64_t n, Range* rg) {
     return true;
 }
 
-template <class Op, class T, int V, int U, int SP, bool RED>
+template <class Op, class T, int V, int U, int SP, bool RED, int THREADS = 256, int MINB = 1>
 fvb_status launch_fixed(const Planes<T, Op::NIN, Op::NOUT>& pl, const Consts<T>& k,
                         const Range& rg, typename Bits<T>::U* red, cudaStream_t stream) {
-    auto kern = pointwise_kernel<Op, T, V, U, SP, RED>;
-    static const int per_sm = resident_ctas(kern);
-    const uint64_t threads = 256;
+    auto kern = pointwise_kernel<Op, T, V, U, SP, RED, THREADS, MINB>;
+    static const int per_sm = resident_ctas(kern, THREADS);
+    const uint64_t threads = THREADS;
     const uint64_t want = (rg.groups + threads * U - 1) / (threads * U);
     const uint64_t cap = uint64_t(device_sm_count()) * uint64_t(per_sm);
     uint64_t grid = want < cap ? want : cap;
@@ -130,29 +135,27 @@ fvb_status launch_op(const T* const* in, T* const* out, uint64_t n, const Consts
     constexpr int VD = vec32<T>();
     const Tuning& t = tuning();
     Range rg;
-    if (TUNABLE) {
+    if constexpr (TUNABLE) {
+      if (t.any()) {
+        // Sweep variants for the headline kernels (FVB_* environment; the
+        // unset defaults below are the measured best).
         const int v = t.vec ? t.vec : VD;
         const int u = t.unroll == 2 ? 2 : 1;
-        const int sp = t.store;
-#define FVB_TRY(VV, UU, SS)                                                          \
-    if (v == VV && u == UU && sp == SS && plan_range<T, VV>(ptrs, np, n, &rg))       \
-        return launch_fixed<Op, T, VV, UU, SS, RED>(pl, k, rg, red, stream);
-#define FVB_TRY_V(VV)     \
-    FVB_TRY(VV, 1, 0)     \
-    FVB_TRY(VV, 1, 1)     \
-    FVB_TRY(VV, 1, 2)     \
-    FVB_TRY(VV, 2, 0)     \
-    FVB_TRY(VV, 2, 1)     \
-    FVB_TRY(VV, 2, 2)
-        if constexpr (sizeof(T) == 8) {
-            FVB_TRY_V(2)
-            FVB_TRY_V(4)
-        } else {
-            FVB_TRY_V(4)
-            FVB_TRY_V(8)
-        }
-#undef FVB_TRY_V
+        const int thr = t.threads ? t.threads : 256;
+        const int mb = t.min_blocks ? t.min_blocks : 1;
+#define FVB_TRY(VV, UU, TT, MB)                                                              \
+    if (v == VV && u == UU && thr == TT && mb == MB && plan_range<T, VV>(ptrs, np, n, &rg)) \
+        return launch_fixed<Op, T, VV, UU, kStoreStreaming, RED, TT, MB>(pl, k, rg, red, stream);
+#define FVB_TRY_U(VV, TT, MB) FVB_TRY(VV, 1, TT, MB) FVB_TRY(VV, 2, TT, MB)
+        FVB_TRY_U(VD, 128, 1)
+        FVB_TRY_U(VD, 128, 4)
+        FVB_TRY_U(VD, 256, 1)
+        FVB_TRY_U(VD, 256, 2)
+        FVB_TRY_U(VD, 512, 1)
+        FVB_TRY(VD / 2, 1, 256, 1)
+#undef FVB_TRY_U
 #undef FVB_TRY
+      }
     }
     if (plan_range<T, VD>(ptrs, np, n, &rg))
         return launch_fixed<Op, T, VD, 1, kStoreStreaming, RED>(pl, k, rg, red, stream);

@@ -270,8 +270,8 @@ __device__ __forceinline__ void point_scalar(const Planes<T, Op::NIN, Op::NOUT>&
 }
 
 // REDUCE: atomically max the block's lambda bits into *red.
-template <class Op, class T, int V, int U, int SP, bool REDUCE>
-__global__ void __launch_bounds__(256)
+template <class Op, class T, int V, int U, int SP, bool REDUCE, int THREADS = 256, int MINB = 1>
+__global__ void __launch_bounds__(THREADS, MINB)
     pointwise_kernel(const Planes<T, Op::NIN, Op::NOUT> pl, const Consts<T> k, const Range rg,
                      typename Bits<T>::U* __restrict__ red) {
     using Bu = typename Bits<T>::U;
