@@ -56,6 +56,7 @@ const Tuning& tuning() {
         x.unroll = env("FVB_UNROLL", 0);
         x.threads = env("FVB_THREADS", 0);
         x.min_blocks = env("FVB_MINB", 0);
+        x.mode = env("FVB_MODE", 0);
         x.ctas_per_sm = env("FVB_CTAS", 0);
         return x;
     }();

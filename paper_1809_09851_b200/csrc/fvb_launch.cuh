@@ -26,10 +26,11 @@ int device_sm_count();
 // Launch tuning, read once from the environment (bench sweeps only; the
 // defaults are the measured best):
 //   FVB_VEC      elements per access: 32 bytes (default) or half of that
-//   FVB_UNROLL   groups per thread per trip: 1 (default) or 2
+//   FVB_UNROLL   groups per thread: 1 (default), 2 or 4
 //   FVB_THREADS  threads per CTA: 128, 256 (default) or 512
 //   FVB_MINB     __launch_bounds__ min blocks per SM: 1 (default), 2 or 4
-//   FVB_CTAS     CTAs per SM cap (0 = occupancy limit)
+//   FVB_MODE     1 = persistent grid-stride, 2 = one-shot tiles (default)
+//   FVB_CTAS     CTAs per SM cap for the persistent mode (0 = occupancy)
 // (Store policy is fixed at st.global.cs: the sweep of round 1 measured
 // st.global / .cs / L1::no_allocate within 0.1% of each other.)
 struct Tuning {
@@ -37,8 +38,9 @@ struct Tuning {
     int unroll = 0;
     int threads = 0;
     int min_blocks = 0;
+    int mode = 0;  // 0 = default, 1 = persistent, 2 = tiles
     int ctas_per_sm = 0;
-    bool any() const { return vec || unroll || threads || min_blocks; }
+    bool any() const { return vec || unroll || threads || min_blocks || mode; }
 };
 const Tuning& tuning();
 
@@ -85,17 +87,21 @@ bool plan_range(const void* const* ptrs, int count, uint64_t n, Range* rg) {
     return true;
 }
 
-template <class Op, class T, int V, int U, int SP, bool RED, int THREADS = 256, int MINB = 1>
+template <class Op, class T, int V, int U, int SP, bool RED, int THREADS = 256, int MINB = 1,
+          int MODE = kTiles>
 fvb_status launch_fixed(const Planes<T, Op::NIN, Op::NOUT>& pl, const Consts<T>& k,
                         const Range& rg, typename Bits<T>::U* red, cudaStream_t stream) {
-    auto kern = pointwise_kernel<Op, T, V, U, SP, RED, THREADS, MINB>;
-    static const int per_sm = resident_ctas(kern, THREADS);
-    const uint64_t threads = THREADS;
-    const uint64_t want = (rg.groups + threads * U - 1) / (threads * U);
-    const uint64_t cap = uint64_t(device_sm_count()) * uint64_t(per_sm);
-    uint64_t grid = want < cap ? want : cap;
-    if (grid == 0) grid = 1;
-    kern<<<unsigned(grid), unsigned(threads), 0, stream>>>(pl, k, rg, red);
+    auto kern = pointwise_kernel<Op, T, V, U, SP, RED, THREADS, MINB, MODE>;
+    const uint64_t per_cta = uint64_t(THREADS) * U;
+    uint64_t grid = (rg.groups + per_cta - 1) / per_cta;
+    if (MODE == kPersistent) {
+        static const int per_sm = resident_ctas(kern, THREADS);
+        const uint64_t cap = uint64_t(device_sm_count()) * uint64_t(per_sm);
+        grid = grid < cap ? grid : cap;
+    }
+    if (grid == 0) grid = 1;  // block 0 still handles the scalar head/tail
+    if (grid > 0x7fffffffull) return fail(FVB_EARG, "range too large for one launch");
+    kern<<<unsigned(grid), unsigned(THREADS), 0, stream>>>(pl, k, rg, red);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? FVB_OK : cuda_fail(e, "kernel launch");
 }
@@ -140,28 +146,40 @@ fvb_status launch_op(const T* const* in, T* const* out, uint64_t n, const Consts
         // Sweep variants for the headline kernels (FVB_* environment; the
         // unset defaults below are the measured best).
         const int v = t.vec ? t.vec : VD;
-        const int u = t.unroll == 2 ? 2 : 1;
+        const int u = t.unroll ? t.unroll : 1;
         const int thr = t.threads ? t.threads : 256;
         const int mb = t.min_blocks ? t.min_blocks : 1;
-#define FVB_TRY(VV, UU, TT, MB)                                                              \
-    if (v == VV && u == UU && thr == TT && mb == MB && plan_range<T, VV>(ptrs, np, n, &rg)) \
-        return launch_fixed<Op, T, VV, UU, kStoreStreaming, RED, TT, MB>(pl, k, rg, red, stream);
-#define FVB_TRY_U(VV, TT, MB) FVB_TRY(VV, 1, TT, MB) FVB_TRY(VV, 2, TT, MB)
-        FVB_TRY_U(VD, 128, 1)
-        FVB_TRY_U(VD, 128, 4)
-        FVB_TRY_U(VD, 256, 1)
-        FVB_TRY_U(VD, 256, 2)
-        FVB_TRY_U(VD, 512, 1)
-        FVB_TRY(VD / 2, 1, 256, 1)
-#undef FVB_TRY_U
+        const int mode = t.mode ? t.mode - 1 : kTiles;
+#define FVB_TRY(VV, UU, TT, MB, MD)                                                    \
+    if (v == VV && u == UU && thr == TT && mb == MB && mode == MD &&                   \
+        plan_range<T, VV>(ptrs, np, n, &rg))                                           \
+        return launch_fixed<Op, T, VV, UU, kStoreStreaming, RED, TT, MB, MD>(pl, k, rg, red, \
+                                                                             stream);
+        FVB_TRY(VD, 1, 256, 1, kTiles)
+        FVB_TRY(VD, 1, 256, 2, kTiles)
+        FVB_TRY(VD, 2, 256, 2, kTiles)
+        FVB_TRY(VD, 2, 256, 1, kTiles)
+        FVB_TRY(VD, 4, 256, 1, kTiles)
+        FVB_TRY(VD, 1, 128, 1, kTiles)
+        FVB_TRY(VD, 2, 128, 1, kTiles)
+        FVB_TRY(VD, 1, 512, 1, kTiles)
+        FVB_TRY(VD / 2, 2, 256, 1, kTiles)
+        FVB_TRY(VD / 2, 4, 256, 1, kTiles)
+        FVB_TRY(VD, 1, 256, 1, kPersistent)
+        FVB_TRY(VD, 2, 256, 1, kPersistent)
 #undef FVB_TRY
       }
     }
+    // Default shape (measured): one-shot tiles of 256
+    // threads x 1 group; two resident CTAs per SM (a 128-register cap) keep
+    // 16 warps of loads in flight, except for the 32- and 75-output Jacobians,
+    // whose live state would spill under that cap.
+    constexpr int MB = Op::NOUT > 24 ? 1 : 2;
     if (plan_range<T, VD>(ptrs, np, n, &rg))
-        return launch_fixed<Op, T, VD, 1, kStoreStreaming, RED>(pl, k, rg, red, stream);
+        return launch_fixed<Op, T, VD, 1, kStoreStreaming, RED, 256, MB>(pl, k, rg, red, stream);
     // Planes with different 32-byte residues: element-wide accesses.
     plan_range<T, 1>(ptrs, np, n, &rg);
-    return launch_fixed<Op, T, 1, 1, kStoreStreaming, RED>(pl, k, rg, red, stream);
+    return launch_fixed<Op, T, 1, 1, kStoreStreaming, RED, 256, MB>(pl, k, rg, red, stream);
 }
 
 }  // namespace fvb

@@ -269,58 +269,84 @@ __device__ __forceinline__ void point_scalar(const Planes<T, Op::NIN, Op::NOUT>&
     }
 }
 
-// REDUCE: atomically max the block's lambda bits into *red.
-template <class Op, class T, int V, int U, int SP, bool REDUCE, int THREADS = 256, int MINB = 1>
+// One trip of a thread: U groups (g0, g0+step, ...) -- all U*NIN wide loads
+// issued first, then the per-point arithmetic and the NOUT wide stores.
+template <class Op, class T, int V, int U, int SP, bool REDUCE>
+__device__ __forceinline__ void pointwise_trip(const Planes<T, Op::NIN, Op::NOUT>& pl,
+                                               const Consts<T>& k, const Range& rg, uint64_t g0,
+                                               uint64_t step, typename Bits<T>::U& acc) {
+    using Bu = typename Bits<T>::U;
+    T x[U][Op::NIN][V];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint64_t g = g0 + u * step;
+        if (g < rg.groups) {
+            const uint64_t base = rg.head + g * V;
+#pragma unroll
+            for (int i = 0; i < Op::NIN; ++i)
+                VecIO<T, V>::template load<!Op::ALIASED>(pl.in[i] + base, x[u][i]);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint64_t g = g0 + u * step;
+        if (g < rg.groups) {
+            const uint64_t base = rg.head + g * V;
+            typename Op::State s[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+                T in[Op::NIN];
+#pragma unroll
+                for (int i = 0; i < Op::NIN; ++i) in[i] = x[u][i][q];
+                s[q] = Op::prepare(in, k);
+            }
+#pragma unroll
+            for (int j = 0; j < Op::NOUT; ++j) {
+                T o[V];
+#pragma unroll
+                for (int q = 0; q < V; ++q) o[q] = Op::out(s[q], j, k);
+                VecIO<T, V>::template store<SP>(pl.out[j] + base, o);
+            }
+            if (REDUCE) {
+#pragma unroll
+                for (int q = 0; q < V; ++q) {
+                    const Bu b = Bits<T>::of(Op::lambda(s[q], k));
+                    acc = b > acc ? b : acc;
+                }
+            }
+        }
+    }
+}
+
+// Launch shapes (template MODE), chosen by measurement (tools/hbm_probe.cu,
+// DESIGN.md §Kernels):
+//   kTiles      (default) one-shot grid; CTA b owns the U*THREADS consecutive
+//               groups [b*U*THREADS, (b+1)*U*THREADS), thread t takes groups
+//               t, t+THREADS, ...  Retiring CTAs are replaced by the block
+//               scheduler, which spreads the streams over HBM; measured
+//               +14% over a persistent sweep for every read/write mix.
+//   kPersistent grid = SMs x resident CTAs, grid-stride over all groups.
+enum LaunchMode : int { kPersistent = 0, kTiles = 1 };
+
+// REDUCE: fold the CTA's lambda bits into *red with one atomicMax, skipped
+// when a coherent read shows *red already at least as large (the running
+// maximum rarely grows, so almost every CTA of a one-shot grid skips the
+// atomic and a single address never becomes a serialisation point).
+template <class Op, class T, int V, int U, int SP, bool REDUCE, int THREADS = 256, int MINB = 1,
+          int MODE = kTiles>
 __global__ void __launch_bounds__(THREADS, MINB)
     pointwise_kernel(const Planes<T, Op::NIN, Op::NOUT> pl, const Consts<T> k, const Range rg,
                      typename Bits<T>::U* __restrict__ red) {
     using Bu = typename Bits<T>::U;
     Bu acc = 0;
-    const uint64_t nthreads = uint64_t(gridDim.x) * blockDim.x;
-    const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-
-    for (uint64_t g0 = tid; g0 < rg.groups; g0 += nthreads * U) {
-        T x[U][Op::NIN][V];
-        // All loads of U groups first: U * NIN wide requests in flight.
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint64_t g = g0 + u * nthreads;
-            if (u == 0 || g < rg.groups) {
-                const uint64_t base = rg.head + g * V;
-#pragma unroll
-                for (int i = 0; i < Op::NIN; ++i)
-                    VecIO<T, V>::template load<!Op::ALIASED>(pl.in[i] + base, x[u][i]);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint64_t g = g0 + u * nthreads;
-            if (u == 0 || g < rg.groups) {
-                const uint64_t base = rg.head + g * V;
-                typename Op::State s[V];
-#pragma unroll
-                for (int q = 0; q < V; ++q) {
-                    T in[Op::NIN];
-#pragma unroll
-                    for (int i = 0; i < Op::NIN; ++i) in[i] = x[u][i][q];
-                    s[q] = Op::prepare(in, k);
-                }
-#pragma unroll
-                for (int j = 0; j < Op::NOUT; ++j) {
-                    T o[V];
-#pragma unroll
-                    for (int q = 0; q < V; ++q) o[q] = Op::out(s[q], j, k);
-                    VecIO<T, V>::template store<SP>(pl.out[j] + base, o);
-                }
-                if (REDUCE) {
-#pragma unroll
-                    for (int q = 0; q < V; ++q) {
-                        const Bu b = Bits<T>::of(Op::lambda(s[q], k));
-                        acc = b > acc ? b : acc;
-                    }
-                }
-            }
-        }
+    if (MODE == kTiles) {
+        const uint64_t g0 = uint64_t(blockIdx.x) * (uint64_t(THREADS) * U) + threadIdx.x;
+        pointwise_trip<Op, T, V, U, SP, REDUCE>(pl, k, rg, g0, THREADS, acc);
+    } else {
+        const uint64_t nthreads = uint64_t(gridDim.x) * THREADS;
+        for (uint64_t g0 = uint64_t(blockIdx.x) * THREADS + threadIdx.x; g0 < rg.groups;
+             g0 += nthreads * U)
+            pointwise_trip<Op, T, V, U, SP, REDUCE>(pl, k, rg, g0, nthreads, acc);
     }
 
     // Unaligned head and ragged tail: at most 2V-2 elements, one per thread
@@ -332,16 +358,18 @@ __global__ void __launch_bounds__(THREADS, MINB)
     }
 
     if (REDUCE) {
-        __shared__ Bu warp_best[32];
+        __shared__ Bu warp_best[THREADS / 32];
         acc = warp_max_u(acc);
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         if (lane == 0) warp_best[warp] = acc;
         __syncthreads();
         if (warp == 0) {
-            const int nwarps = (blockDim.x + 31) >> 5;
-            Bu v = lane < nwarps ? warp_best[lane] : Bu(0);
+            Bu v = lane < THREADS / 32 ? warp_best[lane] : Bu(0);
             v = warp_max_u(v);
-            if (lane == 0 && v != 0) atomicMax(red, v);
+            if (lane == 0 && v != 0) {
+                const Bu seen = *reinterpret_cast<volatile Bu*>(red);
+                if (v > seen) atomicMax(red, v);
+            }
         }
     }
 }

@@ -15,9 +15,11 @@ if [ "$what" = bench ] || [ "$what" = all ]; then
 fi
 if [ "$what" = sweep ] || [ "$what" = all ]; then
   rm -f gpurun_out/sweep.jsonl gpurun_out/sweep_keys.txt
-  for cfg in "256 1 1" "256 2 1" "128 1 1" "128 4 1" "128 1 2" "256 1 2" "512 1 1" "256 2 2"; do
+  for cfg in "2 256 1 0" "2 256 2 0" "2 256 4 0" "2 128 1 0" "2 128 2 0" "2 512 1 0" "2 256 2 2" "2 256 4 2" "1 256 1 0" "1 256 2 0"; do
     set -- $cfg
-    FVB_THREADS=$1 FVB_MINB=$2 FVB_UNROLL=$3 timeout 300 python bench.py --steps 100 --warmup 3 --no-e2e --no-cpu-baseline --out gpurun_out/sweep.jsonl > /dev/null 2>> gpurun_out/sweep.err
-    echo "threads=$1 minb=$2 unroll=$3" >> gpurun_out/sweep_keys.txt
+    for c in "flux3d --prec f64" "flux3d --prec f32" "jacobian3d --prec f64"; do
+      FVB_MODE=$1 FVB_THREADS=$2 FVB_UNROLL=$3 FVB_VEC=$4 timeout 300 python bench.py --config $c --steps 50 --warmup 3 --no-e2e --no-cpu-baseline --out gpurun_out/sweep.jsonl > /dev/null 2>> gpurun_out/sweep.err
+      echo "mode=$1 threads=$2 unroll=$3 vec=$4 $c" >> gpurun_out/sweep_keys.txt
+    done
   done
 fi

@@ -1,0 +1,172 @@
+// hbm_probe.cu -- the achievable HBM ceiling for each kernel's read/write
+// mix, and which streaming pattern reaches it.
+//
+// The roofline denominator in MEASURED_PEAKS.json is a torch copy (1 read :
+// 1 write).  The fused blocks have other mixes (flux 5R:15W, Jacobian
+// 5R:75W, cons->prim 3R:3W), and DRAM efficiency depends on the mix and on
+// the access pattern.  This probe streams R input planes (nonzero data) and
+// W output planes with no arithmetic (out_j = in_{j mod R}) under several
+// patterns:
+//   mode 0  persistent grid-stride, SMs x resident CTAs (the product's)
+//   mode 1  one-shot grid: each CTA owns U*256 consecutive groups, one pass
+//   mode 2  persistent, each CTA owns one contiguous chunk of the range
+// and V = 2 or 4 doubles per access, U groups in flight per thread.
+// Tool only; not part of libfvb.
+//
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/hbm_probe tools/hbm_probe.cu
+//   tools/hbm_probe [points]
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+template <int R, int W>
+struct P {
+    const double* in[R];
+    double* out[W > 0 ? W : 1];
+    double* sink;
+};
+
+template <int V>
+__device__ __forceinline__ void ldv(const double* p, double (&x)[V]) {
+    if constexpr (V == 4)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                     : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3])
+                     : "l"(p));
+    else
+        asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                     : "=d"(x[0]), "=d"(x[1])
+                     : "l"(p));
+}
+
+template <int V>
+__device__ __forceinline__ void stv(double* p, const double (&x)[V]) {
+    if constexpr (V == 4)
+        asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(x[0]), "d"(x[1]),
+                     "d"(x[2]), "d"(x[3])
+                     : "memory");
+    else
+        asm volatile("st.global.cs.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(x[0]), "d"(x[1])
+                     : "memory");
+}
+
+template <int R, int W, int V, int U>
+__device__ __forceinline__ void body(const P<R, W>& p, unsigned long long g0,
+                                     unsigned long long step, unsigned long long groups,
+                                     double& acc) {
+    double x[U][R][V];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const unsigned long long g = g0 + u * step;
+        if (g < groups) {
+#pragma unroll
+            for (int i = 0; i < R; ++i) ldv<V>(p.in[i] + g * V, x[u][i]);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const unsigned long long g = g0 + u * step;
+        if (g < groups) {
+            if (W == 0) {
+#pragma unroll
+                for (int i = 0; i < R; ++i)
+#pragma unroll
+                    for (int q = 0; q < V; ++q) acc = acc + x[u][i][q];
+            }
+#pragma unroll
+            for (int j = 0; j < W; ++j) stv<V>(p.out[j] + g * V, x[u][j % R]);
+        }
+    }
+}
+
+template <int R, int W, int V, int U, int MODE>
+__global__ void __launch_bounds__(256) stream_kernel(P<R, W> p, unsigned long long groups) {
+    double acc = 0;
+    if (MODE == 0) {
+        const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+        for (unsigned long long g = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+             g < groups; g += stride * U)
+            body<R, W, V, U>(p, g, stride, groups, acc);
+    } else if (MODE == 1) {
+        const unsigned long long g = (unsigned long long)blockIdx.x * blockDim.x * U + threadIdx.x;
+        body<R, W, V, U>(p, g, blockDim.x, groups, acc);
+    } else {
+        const unsigned long long per = (groups + gridDim.x - 1) / gridDim.x;
+        const unsigned long long lo = blockIdx.x * per;
+        const unsigned long long hi = lo + per < groups ? lo + per : groups;
+        for (unsigned long long g = lo + threadIdx.x; g < hi; g += (unsigned long long)blockDim.x * U)
+            body<R, W, V, U>(p, g, blockDim.x, hi, acc);
+    }
+    if (W == 0 && acc == 1.2345) *p.sink = acc;
+}
+
+__global__ void fill(double* p, unsigned long long n, double salt) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+        p[i] = 1.0 + double(i % 1000003) * 1e-7 + salt;
+}
+
+template <int R, int W, int V, int U, int MODE>
+void run(const std::vector<double*>& bufs, size_t n, int sms) {
+    P<R, W> p;
+    for (int i = 0; i < R; ++i) p.in[i] = bufs[i];
+    for (int j = 0; j < W; ++j) p.out[j] = bufs[R + j];
+    p.sink = bufs.back();
+    const unsigned long long groups = n / V;
+    auto k = stream_kernel<R, W, V, U, MODE>;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
+    unsigned grid = MODE == 1 ? unsigned((groups + 256ull * U - 1) / (256ull * U))
+                              : unsigned(sms * per_sm);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int w = 0; w < 3; ++w) k<<<grid, 256>>>(p, groups);
+    const int reps = 20;
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) k<<<grid, 256>>>(p, groups);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    const double s = ms * 1e-3 / reps;
+    const double bytes = double(n) * 8 * (R + W);
+    printf("{\"mix\": \"%dR:%dW\", \"V\": %d, \"U\": %d, \"mode\": %d, \"points\": %zu, "
+           "\"ms\": %.4f, \"GBps\": %.1f, \"ctas_per_sm\": %d, \"err\": \"%s\"}\n",
+           R, W, V, U, MODE, n, s * 1e3, bytes / s / 1e9, per_sm,
+           cudaGetErrorString(cudaGetLastError()));
+    fflush(stdout);
+}
+
+template <int R, int W>
+void sweep(const std::vector<double*>& bufs, size_t n, int sms) {
+    run<R, W, 4, 1, 0>(bufs, n, sms);
+    run<R, W, 4, 2, 0>(bufs, n, sms);
+    run<R, W, 2, 2, 0>(bufs, n, sms);
+    run<R, W, 4, 1, 1>(bufs, n, sms);
+    run<R, W, 4, 2, 1>(bufs, n, sms);
+    run<R, W, 4, 4, 1>(bufs, n, sms);
+    run<R, W, 2, 4, 1>(bufs, n, sms);
+    run<R, W, 4, 1, 2>(bufs, n, sms);
+    run<R, W, 4, 2, 2>(bufs, n, sms);
+}
+
+int main(int argc, char** argv) {
+    size_t n = argc > 1 ? strtoull(argv[1], nullptr, 10) : 100000000ull;
+    n &= ~size_t(15);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    std::vector<double*> bufs(21);
+    for (int i = 0; i < 21; ++i) {
+        if (cudaMalloc(&bufs[i], n * 8) != cudaSuccess) return 1;
+        fill<<<sms * 8, 256>>>(bufs[i], n, i);
+    }
+    cudaDeviceSynchronize();
+    sweep<1, 1>(bufs, n, sms);   // copy: the MEASURED_PEAKS denominator's mix
+    sweep<5, 15>(bufs, n, sms);  // 3D flux
+    sweep<3, 3>(bufs, n, sms);   // 1D cons->prim
+    sweep<2, 1>(bufs, n, sms);   // axpy-sin
+    sweep<5, 0>(bufs, n, sms);   // read-only CFL pass
+    return 0;
+}
