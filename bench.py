@@ -193,6 +193,7 @@ def device_run(a, rank, world, local):
     import torch
 
     import paper_1809_09851_b200 as fvb
+    from paper_1809_09851_b200 import shard
 
     dim, n_in, n_out, n_default, desc = CONFIGS[a.config]
     n = a.n or n_default
@@ -208,7 +209,7 @@ def device_run(a, rank, world, local):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.Stream(device=dev)
-    first = rank * n  # weak scaling: this rank's global slice [r*n, (r+1)*n)
+    first, _ = shard.weak_slice(rank, n)  # weak scaling: global slice [r*n, (r+1)*n)
     dt = torch.float64 if prec else torch.float32
 
     with torch.cuda.stream(stream):
@@ -238,7 +239,7 @@ def device_run(a, rank, world, local):
         if a.config == "jacobian3d" and dist is not None:
             with torch.cuda.stream(stream):
                 lam_global.copy_(lam)
-                dist.all_reduce(lam_global, op=dist.ReduceOp.MAX)
+                shard.allreduce_max(lam_global)
 
     for _ in range(a.warmup):
         step()

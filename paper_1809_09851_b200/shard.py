@@ -1,0 +1,49 @@
+"""Multi-GPU plumbing for the sharded path.
+
+Every point is independent and there is no stencil, so the index range
+shards into contiguous slices with no halo: one process per GPU, each owning
+one slice.  The only exchange on the whole path is the CFL maximum of the
+Jacobian/wave-speed pass: one 8-byte all-reduce(MAX) (NCCL over NVLink on
+B200, gloo in the CPU tests).  The maximum is exact and order-independent,
+so results are bitwise invariant to the GPU count.
+"""
+
+from __future__ import annotations
+
+
+def slice_bounds(rank: int, world: int, n_total: int):
+    """Rank r's share of a fixed global range (strong scaling):
+    [floor(r*N/G), floor((r+1)*N/G)).  Ragged N (N mod G != 0, N < G, N in
+    {0, 1}) leaves some slices one point longer, or empty."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world {world}")
+    if n_total < 0:
+        raise ValueError("negative range")
+    return rank * n_total // world, (rank + 1) * n_total // world
+
+
+def weak_slice(rank: int, n_per_rank: int):
+    """Rank r's slice when every GPU owns a fixed n (weak scaling):
+    [r*n, (r+1)*n) of the global sequence."""
+    return rank * n_per_rank, (rank + 1) * n_per_rank
+
+
+def allreduce_max(t, group=None):
+    """In-place all-reduce(MAX) of a 0-d/1-element tensor over the process
+    group; a no-op without an initialised group (single process)."""
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t
+
+
+def cfl_lambda_max(state, dim, gas=None, stream=None, group=None):
+    """Global CFL wave speed of a sharded conservative state: the fused
+    device reduction over this rank's slice (fvb_wave_speed_max), then the
+    one NCCL all-reduce(MAX).  Returns a 0-d float64 device tensor."""
+    from . import device
+
+    _, lam = device.wave_speed_max(state, dim, gas=gas, stream=stream)
+    lam64 = lam.to(dtype=__import__("torch").float64)
+    return allreduce_max(lam64, group)

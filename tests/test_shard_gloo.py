@@ -1,0 +1,75 @@
+"""The N>1 host logic on CPU: contiguous slices tile the range exactly for
+ragged N, and the CFL maximum reduced across 2 gloo ranks equals the global
+maximum bit for bit (the path's one collective; NCCL on the B200 box)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1809_09851_b200 import shard
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("n", [0, 1, 2, 7, 1000, 10**8 + 3])
+def test_slices_tile_the_range(world, n):
+    prev_hi = 0
+    for r in range(world):
+        lo, hi = shard.slice_bounds(r, world, n)
+        assert lo == prev_hi and hi >= lo
+        assert hi - lo in (n // world, n // world + 1)
+        prev_hi = hi
+    assert prev_hi == n
+
+
+def test_slice_bounds_rejects_bad_rank():
+    with pytest.raises(ValueError):
+        shard.slice_bounds(2, 2, 10)
+
+
+def test_weak_slices_are_disjoint_and_contiguous():
+    n = 1000
+    spans = [shard.weak_slice(r, n) for r in range(8)]
+    assert spans[0] == (0, n) and all(spans[i][1] == spans[i + 1][0] for i in range(7))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, n_total, dim, result):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+
+    orc = oracle.oracle()
+    lo, hi = shard.slice_bounds(rank, world, n_total)
+    # each rank generates its own slice from the global index, exactly as the
+    # device generator does on each GPU
+    s = orc.random_state(dim, hi - lo, seed=0x5EED, first=lo)
+    local = orc.wave_speed_max(dim, s) if hi > lo else 0.0
+    t = torch.tensor([local], dtype=torch.float64)
+    shard.allreduce_max(t)
+    result[rank] = t.item()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_total", [1, 10_001])
+def test_cfl_allreduce_max_gloo_world2(orc, n_total):
+    world, dim = 2, 3
+    mgr = mp.Manager()
+    result = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), n_total, dim, result), nprocs=world, join=True)
+    whole = orc.wave_speed_max(dim, orc.random_state(dim, n_total, seed=0x5EED))
+    assert [result[r] for r in range(world)] == [whole] * world
+    # and bitwise: the global max is one of the per-point values
+    assert np.float64(whole).tobytes() == np.float64(result[0]).tobytes()
