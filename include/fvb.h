@@ -171,9 +171,17 @@ FVB_API fvb_status fvb_synth_uniform(uint8_t prec, uint64_t seed, uint64_t first
 typedef struct fvb_kernel fvb_kernel;
 typedef fvb_status (*fvb_kernel_fn)(const fvb_kernel* self, uint64_t begin, uint64_t end,
                                     void* const* args, void* stream);
+/* For blocks that carry a CFL wave speed (Jacobian, wave speed): the same
+ * pass, additionally max-accumulating lambda over [begin, end) into the
+ * DEVICE scalar lambda_max (of the kernel's precision).  It accumulates --
+ * the caller zeroes it once -- so a range split into chunks reduces to the
+ * same value.  For the wave-speed block args[0] may be NULL (reduce only). */
+typedef fvb_status (*fvb_kernel_reduce_fn)(const fvb_kernel* self, uint64_t begin, uint64_t end,
+                                           void* const* args, void* lambda_max, void* stream);
 
 struct fvb_kernel {
     fvb_kernel_fn fn;
+    fvb_kernel_reduce_fn reduce; /* NULL unless the block has a CFL reduction */
     uint32_t n_outputs;  /* leading output slots in args                      */
     uint32_t n_inputs;   /* distinct leaf slots after them                    */
     uint32_t n_consts;   /* valid entries of consts                           */

@@ -100,8 +100,13 @@ class KernelStruct(ctypes.Structure):
 KERNEL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(KernelStruct), ctypes.c_uint64,
                              ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p)
 
+KERNEL_REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(KernelStruct), ctypes.c_uint64,
+                                    ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p),
+                                    ctypes.c_void_p, ctypes.c_void_p)
+
 KernelStruct._fields_ = [
     ("fn", KERNEL_FN),
+    ("reduce", KERNEL_REDUCE_FN),
     ("n_outputs", ctypes.c_uint32),
     ("n_inputs", ctypes.c_uint32),
     ("n_consts", ctypes.c_uint32),

@@ -282,6 +282,37 @@ fvb_status entry(const fvb_kernel* k, uint64_t begin, uint64_t end, void* const*
                                           static_cast<cudaStream_t>(stream));
 }
 
+// The reduce entry: same pass plus the CFL max, accumulated into *red.
+template <class Op, class T>
+fvb_status entry_reduce(const fvb_kernel* k, uint64_t begin, uint64_t end, void* const* args,
+                        void* red, void* stream) {
+    if (!k || !args || !red) return fail(FVB_EARG, "NULL kernel, argument block or lambda_max");
+    if (end < begin) return fail(FVB_EARG, "end < begin");
+    const T* in[Op::NIN];
+    for (int i = 0; i < Op::NIN; ++i) {
+        const int s = k->in_slot[i];
+        if (s < 0 || uint32_t(s) >= k->n_inputs || !args[k->n_outputs + s])
+            return fail(FVB_EARG, "NULL or missing leaf slot");
+        in[i] = static_cast<const T*>(args[k->n_outputs + s]) + begin;
+    }
+    T* out[Op::NOUT > 0 ? Op::NOUT : 1];
+    for (int j = 0; j < Op::NOUT; ++j) {
+        if (!args[j]) return fail(FVB_EARG, "NULL output slot");
+        out[j] = static_cast<T*>(args[j]) + begin;
+    }
+    return launch_op<Op, T, true, false>(in, out, end - begin, consts_of<T>(k),
+                                         static_cast<typename Bits<T>::U*>(red),
+                                         static_cast<cudaStream_t>(stream));
+}
+
+// Wave speed: per-point lambda when args[0] is set, reduction only otherwise.
+template <class T, int D>
+fvb_status wave_reduce(const fvb_kernel* k, uint64_t begin, uint64_t end, void* const* args,
+                       void* red, void* stream) {
+    if (args && args[0]) return entry_reduce<WaveSpeedOp<T, D, 1>, T>(k, begin, end, args, red, stream);
+    return entry_reduce<WaveSpeedOp<T, D, 0>, T>(k, begin, end, args, red, stream);
+}
+
 struct Pattern {
     std::string name;
     std::string text;                // key with named constant wildcards
@@ -290,6 +321,7 @@ struct Pattern {
     uint32_t n_outputs;
     uint8_t prec, dim;
     fvb_kernel_fn fn;
+    fvb_kernel_reduce_fn reduce = nullptr;
 };
 
 std::vector<std::string> cons_names(int d) {
@@ -334,10 +366,12 @@ void add_fluid(std::vector<Pattern>& ps) {
     block("cons2prim_c", D + 2, 1, prim_items(u, true), cn, entry<Cons2PrimOp<T, D>, T>);
     block("prim2cons", D + 1, 1, cons_items(D), prim_names(D), entry<Prim2ConsOp<T, D>, T>);
     block("jacobian", D * (D + 2), D + 2, jacobian_items(u), cn, entry<JacobianOp<T, D>, T>);
+    ps.back().reduce = entry_reduce<JacobianOp<T, D>, T>;
     single("pressure", derived_p(u), cn, entry<SliceOp<Cons2PrimOp<T, D>, D, 1>, T>);
     single("sound_speed", sound_speed(u), cn, entry<SliceOp<Cons2PrimOp<T, D>, D + 1, 1>, T>);
     single("v_mag2", v_mag2(u), cn, entry<VMag2Op<T, D>, T>);
     single("wave_speed", wave_speed(u), cn, entry<WaveSpeedOp<T, D, 1>, T>);
+    ps.back().reduce = wave_reduce<T, D>;
 }
 
 template <class T>
@@ -449,6 +483,7 @@ fvb_status fvb_lookup(const char* key, fvb_kernel* out) {
         fvb_kernel k;
         std::memset(&k, 0, sizeof k);
         k.fn = p.fn;
+        k.reduce = p.reduce;
         k.n_outputs = p.n_outputs;
         k.n_inputs = uint32_t(p.slots.size());
         k.n_consts = kNumConsts;

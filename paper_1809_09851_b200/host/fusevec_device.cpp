@@ -1,0 +1,680 @@
+// fusevec_device.cpp -- see fusevec_device.hpp.
+//
+// Compiled against the reference's public headers (the maintainer's
+// fusevec, or in our tests the reference built as namespace fvref), linked
+// with libfvb.so and the CUDA runtime.
+#include "fusevec_device.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+
+#include "fvb.h"
+
+namespace fusevec {
+
+// ---------------------------------------------------------------------------
+// New fluid expression objects, built only from the public Expr API in the
+// style of proj/src/fluid.cpp (SURVEY Appendix A gives the operation order;
+// the fused kernels and the registry patterns mirror exactly these trees).
+// ---------------------------------------------------------------------------
+
+namespace {
+
+double gm1_of(const EosSpec& eos) { return (eos.R() / eos.cv()).value(); }
+
+void require_conservative(const StateSet& u, const char* what) {
+    if (u.formulation() != Formulation::Conservative)
+        throw BadMap(std::string(what) + " needs a conservative state");
+}
+
+}  // namespace
+
+Expr derived_c(const StateSet& u) {
+    // A.2: elem_sqrt((constant(gamma, p) * p) / rho)
+    Expr p = derived_p(u);
+    const Expr& rho = u.field(VarKind::Density);
+    return elem_sqrt((constant(u.eos().gamma_value(), p) * p) / rho);
+}
+
+Expr wave_speed(const StateSet& u) {
+    // A.4: elem_sqrt(derived_v_mag2(u)) + c
+    require_conservative(u, "wave_speed");
+    return elem_sqrt(derived_v_mag2(u)) + derived_c(u);
+}
+
+BlockExpr inviscid_flux_jacobian(const StateSet& u) {
+    // A.3, items [k][r][c] of a (d*(d+2)) x (d+2) row-major block.
+    require_conservative(u, "inviscid_flux_jacobian");
+    const std::size_t d = u.dim(), w = d + 2;
+    const Expr& rho = u.field(VarKind::Density);
+    const Expr& rho_E = u.field(VarKind::TotalEnergy);
+    Expr p = derived_p(u);
+    std::vector<Expr> v(d);
+    for (std::size_t j = 0; j < d; ++j) v[j] = u.field(1 + j) / rho;
+    Expr q2;
+    for (std::size_t j = 0; j < d; ++j) q2 = q2.valid() ? q2 + v[j] * v[j] : v[j] * v[j];
+    Expr H = (rho_E + p) / rho;
+    const double gm1 = gm1_of(u.eos());
+    Expr phi = constant(0.5, q2) * (constant(gm1, q2) * q2);
+    auto lit = [&](double x) { return constant(x, rho); };
+
+    std::vector<BlockItem> items;
+    items.reserve(d * w * w);
+    for (std::size_t k = 0; k < d; ++k) {
+        for (std::size_t c = 0; c < w; ++c) items.push_back(BlockItem(lit(c == 1 + k ? 1.0 : 0.0)));
+        for (std::size_t i = 0; i < d; ++i) {
+            items.push_back(BlockItem(i == k ? phi - v[i] * v[k] : -(v[i] * v[k])));
+            for (std::size_t j = 0; j < d; ++j) {
+                Expr acc;
+                if (i == j) acc = v[k];
+                if (j == k) acc = acc.valid() ? acc + v[i] : v[i];
+                if (i == k) {
+                    Expr t = -(constant(gm1, v[j]) * v[j]);
+                    acc = acc.valid() ? acc + t : t;
+                }
+                items.push_back(BlockItem(acc.valid() ? acc : lit(0.0)));
+            }
+            items.push_back(BlockItem(lit(i == k ? gm1 : 0.0)));
+        }
+        items.push_back(BlockItem(v[k] * (phi - H)));
+        for (std::size_t j = 0; j < d; ++j) {
+            Expr ujuk = v[j] * v[k];
+            items.push_back(BlockItem(j == k ? H - constant(gm1, ujuk) * ujuk
+                                             : -(constant(gm1, ujuk) * ujuk)));
+        }
+        items.push_back(BlockItem(constant(u.eos().gamma_value(), v[k]) * v[k]));
+    }
+    return BlockExpr(d * w, w, std::move(items));
+}
+
+namespace device {
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw DeviceError(std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                          cudaGetErrorString(e) + ")");
+}
+
+void fvb_check(fvb_status st) {
+    if (st == FVB_OK) return;
+    std::string msg = fvb_last_error();
+    switch (st) {
+        case FVB_ELEN: throw LengthMismatch(msg);
+        case FVB_EUNSUPPORTED: throw UnsupportedExpression(msg);
+        case FVB_ECUDA: throw DeviceError(msg);
+        default: throw Error(msg);
+    }
+}
+
+char prec_char(Precision p) { return p == Precision::f32 ? 's' : 'd'; }
+
+double narrow(double v, Precision p) {
+    return p == Precision::f32 ? static_cast<double>(static_cast<float>(v)) : v;
+}
+
+// Leaf slots across one key: distinct DenseVectors in first-appearance
+// left-to-right DFS order (proj/src/backend_jit.cpp:78-99).
+struct Slots {
+    std::vector<const DenseVector*> v;
+    std::size_t of(const DenseVector* x) {
+        for (std::size_t i = 0; i < v.size(); ++i)
+            if (v[i] == x) return i;
+        v.push_back(x);
+        return v.size() - 1;
+    }
+};
+
+// key_node (proj/src/backend_jit.cpp:112-155): same grammar, same order.
+void key_node(const ExprNode& n, Slots& slots, bool& ok, std::string& out) {
+    switch (n.kind) {
+        case NodeKind::Leaf:
+            out += 'L';
+            out += prec_char(n.prec);
+            out += std::to_string(slots.of(n.vec));
+            out += ';';
+            return;
+        case NodeKind::Constant: {
+            const double v = narrow(n.value, n.prec);
+            if (!std::isfinite(v)) ok = false;
+            unsigned long long bits;
+            std::memcpy(&bits, &v, sizeof bits);
+            char buf[32];
+            std::snprintf(buf, sizeof buf, "C%c%016llx;", prec_char(n.prec), bits);
+            out += buf;
+            return;
+        }
+        case NodeKind::Tagged:
+        case NodeKind::Cached:
+            key_node(*n.left, slots, ok, out);
+            return;
+        case NodeKind::Unary:
+            out += 'U';
+            out += std::to_string(static_cast<int>(n.uop));
+            out += prec_char(n.prec);
+            out += '(';
+            key_node(*n.left, slots, ok, out);
+            out += ')';
+            return;
+        case NodeKind::Binary:
+            out += 'B';
+            out += std::to_string(static_cast<int>(n.bop));
+            out += prec_char(n.prec);
+            out += '(';
+            key_node(*n.left, slots, ok, out);
+            out += ',';
+            key_node(*n.right, slots, ok, out);
+            out += ')';
+            return;
+    }
+}
+
+// validate() semantics of proj/src/backend_eval.cpp:236-265.
+void validate(const ExprNode& n, std::size_t len, std::map<int, const DenseVector*>& tags) {
+    switch (n.kind) {
+        case NodeKind::Leaf:
+            if (n.vec->size() != len)
+                throw LengthMismatch("leaf length " + std::to_string(n.vec->size()) +
+                                     " does not match destination length " + std::to_string(len));
+            return;
+        case NodeKind::Constant:
+            return;
+        case NodeKind::Tagged:
+            if (n.left->kind == NodeKind::Leaf) {
+                auto [it, inserted] = tags.emplace(n.tag, n.left->vec);
+                if (!inserted && it->second != n.left->vec)
+                    throw TagConflict("tag " + std::to_string(n.tag) +
+                                      " bound to two different leaves");
+            }
+            validate(*n.left, len, tags);
+            return;
+        case NodeKind::Cached:
+        case NodeKind::Unary:
+            validate(*n.left, len, tags);
+            return;
+        case NodeKind::Binary:
+            validate(*n.left, len, tags);
+            validate(*n.right, len, tags);
+            return;
+    }
+}
+
+const DenseVector* bare_leaf(const ExprNode& n) {
+    if (n.kind == NodeKind::Leaf) return n.vec;
+    if (n.kind == NodeKind::Tagged || n.kind == NodeKind::Cached) return bare_leaf(*n.left);
+    return nullptr;
+}
+
+// One output of a plan: a host vector (staged), a device plane, or neither
+// (a NULL slot: the reduce-only wave-speed pass writes no plane).
+struct Out {
+    DenseVector* host = nullptr;
+    DeviceVector* dev = nullptr;
+    Precision null_prec = Precision::f64;
+    std::size_t null_size = 0;
+    bool is_null() const { return !host && !dev; }
+    Precision prec() const {
+        return host ? host->precision() : dev ? dev->precision() : null_prec;
+    }
+    std::size_t size() const { return host ? host->size() : dev ? dev->size() : null_size; }
+};
+
+struct Plan {
+    fvb_kernel k{};
+    std::vector<const DenseVector*> leaves;
+    std::vector<Out> outs;
+};
+
+// Streams and staging memory reused across calls (per device).
+struct Staging {
+    cudaStream_t s[2] = {nullptr, nullptr};
+    void* buf[2] = {nullptr, nullptr};
+    std::size_t bytes = 0;
+};
+
+Staging& staging(int ordinal) {
+    static std::mutex mu;
+    static std::map<int, std::unique_ptr<Staging>> per;
+    std::lock_guard<std::mutex> lock(mu);
+    auto& p = per[ordinal];
+    if (!p) {
+        p = std::make_unique<Staging>();
+        for (auto& s : p->s) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    }
+    return *p;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
+        if (prev != dev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// Execute a plan over [0, n): resident leaves/outputs in place, host ones
+// staged through the device chunk by chunk on two alternating streams.
+// With red != nullptr the kernel's CFL reduction accumulates into it.
+void run(const DeviceBackend& be, Plan& plan, std::size_t n, void* red) {
+    if (n == 0) return;
+    const std::size_t w = plan.k.prec ? sizeof(double) : sizeof(float);
+    const Precision P = plan.k.prec ? Precision::f64 : Precision::f32;
+    for (const DenseVector* l : plan.leaves)
+        if (l->precision() != P) throw UnsupportedExpression("mixed-precision leaves");
+    for (const Out& o : plan.outs)
+        if (o.prec() != P) throw UnsupportedExpression("destination precision differs");
+
+    DeviceGuard guard(be.ordinal);
+    // which leaves / outputs need staging
+    std::vector<void*> resident_leaf(plan.leaves.size(), nullptr);
+    std::size_t staged = 0;
+    for (std::size_t i = 0; i < plan.leaves.size(); ++i) {
+        DeviceVector* dv = be.residency ? be.residency->find(plan.leaves[i]) : nullptr;
+        if (dv) {
+            if (dv->size() != n || dv->precision() != P)
+                throw LengthMismatch("resident plane does not match its host leaf");
+            resident_leaf[i] = dv->data();
+        } else {
+            ++staged;
+        }
+    }
+    // An output aliasing a staged leaf (in-place evaluate) reuses its buffer.
+    std::vector<long> alias(plan.outs.size(), -1);
+    for (std::size_t j = 0; j < plan.outs.size(); ++j) {
+        if (!plan.outs[j].host) continue;  // device planes and NULL slots need no staging
+        for (std::size_t i = 0; i < plan.leaves.size(); ++i)
+            if (plan.leaves[i] == plan.outs[j].host && !resident_leaf[i]) alias[j] = long(i);
+        if (alias[j] < 0) ++staged;
+    }
+
+    const bool external = be.stream != nullptr;
+    Staging& st = staging(be.ordinal);
+    std::size_t chunk = staged ? std::max<std::size_t>(be.chunk_points & ~std::size_t(63), 64) : n;
+    chunk = std::min(chunk, n);
+    const std::size_t need = staged * chunk * w;
+    if (need > st.bytes) {
+        for (int b = 0; b < 2; ++b) {
+            if (st.buf[b]) {
+                cuda_check(cudaStreamSynchronize(st.s[b]), "staging drain");
+                cuda_check(cudaFree(st.buf[b]), "cudaFree");
+                st.buf[b] = nullptr;
+            }
+            cuda_check(cudaMalloc(&st.buf[b], need), "staging allocation");
+        }
+        st.bytes = need;
+    }
+
+    std::vector<void*> args(plan.outs.size() + plan.leaves.size());
+    for (std::size_t off = 0, c = 0; off < n; off += chunk, ++c) {
+        const std::size_t cnt = std::min(chunk, n - off);
+        const int b = external ? 0 : int(c % 2);
+        cudaStream_t s = external ? static_cast<cudaStream_t>(be.stream) : st.s[b];
+        char* base = static_cast<char*>(st.buf[b]);
+        std::size_t slot = 0;
+        std::vector<void*> leaf_ptr(plan.leaves.size());
+        for (std::size_t i = 0; i < plan.leaves.size(); ++i) {
+            if (resident_leaf[i]) {
+                leaf_ptr[i] = static_cast<char*>(resident_leaf[i]) + off * w;
+            } else {
+                leaf_ptr[i] = base + (slot++) * chunk * w;
+                cuda_check(cudaMemcpyAsync(leaf_ptr[i],
+                                           static_cast<const char*>(plan.leaves[i]->raw()) + off * w,
+                                           cnt * w, cudaMemcpyHostToDevice, s),
+                           "host->device copy");
+            }
+        }
+        for (std::size_t j = 0; j < plan.outs.size(); ++j) {
+            if (plan.outs[j].is_null())
+                args[j] = nullptr;
+            else if (plan.outs[j].dev)
+                args[j] = static_cast<char*>(plan.outs[j].dev->data()) + off * w;
+            else if (alias[j] >= 0)
+                args[j] = leaf_ptr[std::size_t(alias[j])];
+            else
+                args[j] = base + (slot++) * chunk * w;
+        }
+        for (std::size_t i = 0; i < plan.leaves.size(); ++i) args[plan.outs.size() + i] = leaf_ptr[i];
+        if (red)
+            fvb_check(plan.k.reduce(&plan.k, 0, cnt, args.data(), red, s));
+        else
+            fvb_check(plan.k.fn(&plan.k, 0, cnt, args.data(), s));
+        for (std::size_t j = 0; j < plan.outs.size(); ++j)
+            if (plan.outs[j].host)
+                cuda_check(cudaMemcpyAsync(static_cast<char*>(plan.outs[j].host->raw()) + off * w,
+                                           args[j], cnt * w, cudaMemcpyDeviceToHost, s),
+                           "device->host copy");
+    }
+    if (external) {
+        cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(be.stream)), "sync");
+    } else {
+        cuda_check(cudaStreamSynchronize(st.s[0]), "sync");
+        cuda_check(cudaStreamSynchronize(st.s[1]), "sync");
+    }
+}
+
+// Look up the fused kernel for `items` writing `outs`; single items use the
+// reference's expression key, several the block key.
+bool try_plan(const std::vector<Expr>& items, std::vector<Out> outs, std::size_t rows,
+              std::size_t cols, Plan* plan) {
+    std::vector<Precision> dests;
+    for (const Out& o : outs) dests.push_back(o.prec());
+    std::vector<const DenseVector*> leaves;
+    std::string key;
+    if (items.size() == 1) {
+        Slots slots;
+        bool ok = true;
+        key.assign(1, prec_char(dests[0]));
+        key_node(items[0].node(), slots, ok, key);
+        if (!ok) return false;
+        leaves = slots.v;
+    } else {
+        key = block_key(items, dests, rows, cols, &leaves);
+        if (key.empty()) return false;
+    }
+    fvb_kernel k;
+    if (fvb_lookup(key.c_str(), &k) != FVB_OK) return false;
+    if (k.n_outputs != outs.size() || k.n_inputs != leaves.size()) return false;
+    plan->k = k;
+    plan->leaves = std::move(leaves);
+    plan->outs = std::move(outs);
+    return true;
+}
+
+[[noreturn]] void unsupported(const std::vector<Expr>& items) {
+    std::string k = items.size() == 1 ? structural_key(items[0], items[0].result_precision())
+                                      : std::string("block of ") + std::to_string(items.size()) +
+                                            " items";
+    throw UnsupportedExpression("no fused device kernel for " + k.substr(0, 200) +
+                                " (general lowering is not implemented; no CPU fallback)");
+}
+
+// Shared body of the evaluate_block overloads.
+void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, std::size_t cols,
+                const std::vector<Out>& dests_in, void* red, bool need_reduce) {
+    if (e.block_rows() != rows || e.block_cols() != cols)
+        throw ShapeMismatch("block expression shape " + std::to_string(e.block_rows()) + "x" +
+                            std::to_string(e.block_cols()) + " does not match destination " +
+                            std::to_string(rows) + "x" + std::to_string(cols));
+    std::vector<Expr> items;
+    std::vector<Out> outs;
+    std::vector<std::pair<const DenseVector*, Out>> copies;  // bare-leaf items
+    std::size_t idx = 0;
+    for (std::size_t r = 0; r < rows; ++r)
+        for (std::size_t c = 0; c < cols; ++c, ++idx) {
+            const BlockItem& it = e.item(r, c);
+            Expr x;
+            switch (it.kind()) {
+                case ItemKind::Expression: x = it.expr(); break;
+                case ItemKind::Vector: x = leaf(it.vector()); break;
+                default:
+                    throw UnsupportedExpression(
+                        "sparse-matrix block items are not on the device path");
+            }
+            const Out& d = dests_in[idx];
+            std::map<int, const DenseVector*> tags;
+            validate(x.node(), d.size(), tags);
+            // aliased pass-through moves no memory (proj/src/block.cpp:419-422)
+            if (d.host && bare_leaf(x.node()) == d.host) continue;
+            items.push_back(x);
+            outs.push_back(d);
+        }
+    if (items.empty()) return;
+    const std::size_t n = outs[0].size();
+    for (const Out& o : outs)
+        if (o.size() != n) throw LengthMismatch("block destinations have different lengths");
+    Plan plan;
+    if (!try_plan(items, outs, rows, cols, &plan)) {
+        // strip bare-leaf items (plain copies) and retry with the rest
+        std::vector<Expr> rest;
+        std::vector<Out> rest_outs;
+        for (std::size_t i = 0; i < items.size(); ++i) {
+            if (const DenseVector* src = bare_leaf(items[i].node()))
+                copies.push_back({src, outs[i]});
+            else {
+                rest.push_back(items[i]);
+                rest_outs.push_back(outs[i]);
+            }
+        }
+        if (rest.empty() || !try_plan(rest, rest_outs, rest.size(), 1, &plan)) unsupported(items);
+    }
+    if (need_reduce && !plan.k.reduce)
+        throw UnsupportedExpression("block has no fused CFL reduction");
+    run(be, plan, n, red);
+    for (auto& [src, d] : copies) {
+        DeviceGuard guard(be.ordinal);
+        if (d.host)
+            std::memcpy(d.host->raw(), src->raw(), d.host->byte_size());
+        else
+            cuda_check(cudaMemcpy(d.dev->data(), src->raw(), d.dev->byte_size(),
+                                  cudaMemcpyHostToDevice),
+                       "pass-through copy");
+    }
+}
+
+double read_max(void* red, Precision p) {
+    if (p == Precision::f64) {
+        double v;
+        cuda_check(cudaMemcpy(&v, red, sizeof v, cudaMemcpyDeviceToHost), "lambda read-back");
+        return v;
+    }
+    float v;
+    cuda_check(cudaMemcpy(&v, red, sizeof v, cudaMemcpyDeviceToHost), "lambda read-back");
+    return double(v);
+}
+
+struct DeviceScalar {
+    void* p = nullptr;
+    explicit DeviceScalar(int ordinal) {
+        DeviceGuard guard(ordinal);
+        cuda_check(cudaMalloc(&p, 8), "scalar allocation");
+        cuda_check(cudaMemset(p, 0, 8), "scalar reset");
+    }
+    ~DeviceScalar() {
+        if (p) cudaFree(p);
+    }
+};
+
+}  // namespace
+
+// ---- DeviceVector / Residency ------------------------------------------------
+
+DeviceVector::DeviceVector(Precision prec, std::size_t len) : prec_(prec), len_(len) {
+    if (len_) cuda_check(cudaMalloc(&ptr_, byte_size()), "DeviceVector allocation");
+}
+
+DeviceVector::~DeviceVector() {
+    if (ptr_) cudaFree(ptr_);
+}
+
+DeviceVector::DeviceVector(DeviceVector&& o) noexcept : prec_(o.prec_), len_(o.len_), ptr_(o.ptr_) {
+    o.ptr_ = nullptr;
+    o.len_ = 0;
+}
+
+DeviceVector& DeviceVector::operator=(DeviceVector&& o) noexcept {
+    if (this != &o) {
+        if (ptr_) cudaFree(ptr_);
+        prec_ = o.prec_;
+        len_ = o.len_;
+        ptr_ = o.ptr_;
+        o.ptr_ = nullptr;
+        o.len_ = 0;
+    }
+    return *this;
+}
+
+void DeviceVector::upload(const DenseVector& host) {
+    if (host.size() != len_) throw LengthMismatch("upload: length differs");
+    if (host.precision() != prec_) throw Error("upload: precision differs");
+    if (len_) cuda_check(cudaMemcpy(ptr_, host.raw(), byte_size(), cudaMemcpyHostToDevice), "upload");
+}
+
+void DeviceVector::download(DenseVector& host) const {
+    if (host.size() != len_) throw LengthMismatch("download: length differs");
+    if (host.precision() != prec_) throw Error("download: precision differs");
+    if (len_)
+        cuda_check(cudaMemcpy(host.raw(), ptr_, byte_size(), cudaMemcpyDeviceToHost), "download");
+}
+
+DeviceVector make_temp(Precision prec, std::size_t len) { return DeviceVector(prec, len); }
+
+void Residency::bind(const DenseVector& host, DeviceVector& dev) {
+    if (host.size() != dev.size()) throw LengthMismatch("bind: length differs");
+    map_[&host] = &dev;
+}
+
+void Residency::unbind(const DenseVector& host) { map_.erase(&host); }
+
+DeviceVector* Residency::find(const DenseVector* host) const {
+    auto it = map_.find(host);
+    return it == map_.end() ? nullptr : it->second;
+}
+
+// ---- keys ---------------------------------------------------------------------
+
+std::string structural_key(const Expr& e, Precision dest) {
+    Slots slots;
+    bool ok = true;
+    std::string key(1, prec_char(dest));
+    key_node(e.node(), slots, ok, key);
+    return ok ? key : std::string();
+}
+
+std::string block_key(const std::vector<Expr>& items, const std::vector<Precision>& dests,
+                      std::size_t rows, std::size_t cols,
+                      std::vector<const DenseVector*>* leaves) {
+    Slots slots;
+    bool ok = true;
+    std::string key = "G" + std::to_string(rows) + "x" + std::to_string(cols) + ":";
+    for (std::size_t i = 0; i < items.size(); ++i) {
+        if (i) key += '|';
+        key += prec_char(dests[i]);
+        key_node(items[i].node(), slots, ok, key);
+    }
+    if (leaves) *leaves = slots.v;
+    return ok ? key : std::string();
+}
+
+// ---- evaluation -----------------------------------------------------------------
+
+void evaluate(const DeviceBackend& be, const Expr& e, DenseVector& dest) {
+    if (!e.valid()) throw Error("cannot evaluate an empty expression");
+    std::map<int, const DenseVector*> tags;
+    validate(e.node(), dest.size(), tags);
+    if (dest.size() == 0) return;
+    Plan plan;
+    Out o;
+    o.host = &dest;
+    if (!try_plan({e}, {o}, 1, 1, &plan)) unsupported({e});
+    run(be, plan, dest.size(), nullptr);
+}
+
+void evaluate(const DeviceBackend& be, const Expr& e, DeviceVector& dest) {
+    if (!e.valid()) throw Error("cannot evaluate an empty expression");
+    std::map<int, const DenseVector*> tags;
+    validate(e.node(), dest.size(), tags);
+    if (dest.size() == 0) return;
+    Plan plan;
+    Out o;
+    o.dev = &dest;
+    if (!try_plan({e}, {o}, 1, 1, &plan)) unsupported({e});
+    run(be, plan, dest.size(), nullptr);
+}
+
+void evaluate_block(const DeviceBackend& be, const BlockExpr& e, BlockVectorGrid& dest) {
+    std::vector<Out> outs;
+    for (std::size_t r = 0; r < dest.block_rows(); ++r)
+        for (std::size_t c = 0; c < dest.block_cols(); ++c) {
+            Out o;
+            o.host = &dest.item(r, c);
+            outs.push_back(o);
+        }
+    block_impl(be, e, dest.block_rows(), dest.block_cols(), outs, nullptr, false);
+}
+
+void evaluate_block(const DeviceBackend& be, const BlockExpr& e, BlockColVector& dest) {
+    std::vector<Out> outs;
+    for (std::size_t r = 0; r < dest.size(); ++r) {
+        Out o;
+        o.host = &dest.get(r);
+        outs.push_back(o);
+    }
+    block_impl(be, e, dest.size(), 1, outs, nullptr, false);
+}
+
+void evaluate_block(const DeviceBackend& be, const BlockExpr& e, const Tie& dest) {
+    if (dest.dests.size() != e.block_rows() * e.block_cols())
+        throw ShapeMismatch("tie has " + std::to_string(dest.dests.size()) +
+                            " destinations for a " + std::to_string(e.block_rows()) + "x" +
+                            std::to_string(e.block_cols()) + " block");
+    std::vector<Out> outs;
+    for (DeviceVector* d : dest.dests) {
+        Out o;
+        o.dev = d;
+        outs.push_back(o);
+    }
+    block_impl(be, e, e.block_rows(), e.block_cols(), outs, nullptr, false);
+}
+
+double reduce_max(const DeviceBackend& be, const Expr& lambda) {
+    if (!lambda.valid()) throw Error("cannot reduce an empty expression");
+    const Precision P = lambda.result_precision();
+    Slots slots;
+    bool ok = true;
+    std::string key(1, prec_char(P));
+    key_node(lambda.node(), slots, ok, key);
+    Plan plan;
+    if (!ok || fvb_lookup(key.c_str(), &plan.k) != FVB_OK || !plan.k.reduce)
+        throw UnsupportedExpression("reduce_max needs a wave-speed expression (wave_speed(u))");
+    plan.leaves = slots.v;
+    const std::size_t n = plan.leaves.empty() ? 0 : plan.leaves[0]->size();
+    std::map<int, const DenseVector*> tags;
+    validate(lambda.node(), n, tags);
+    Out none;  // NULL output slot: reduce only, no lambda plane
+    none.null_prec = P;
+    none.null_size = n;
+    plan.outs = {none};
+    DeviceScalar red(be.ordinal);
+    run(be, plan, n, red.p);
+    return read_max(red.p, P);
+}
+
+double evaluate_block_cfl(const DeviceBackend& be, const BlockExpr& jacobian,
+                          BlockVectorGrid& dest) {
+    std::vector<Out> outs;
+    for (std::size_t r = 0; r < dest.block_rows(); ++r)
+        for (std::size_t c = 0; c < dest.block_cols(); ++c) {
+            Out o;
+            o.host = &dest.item(r, c);
+            outs.push_back(o);
+        }
+    DeviceScalar red(be.ordinal);
+    block_impl(be, jacobian, dest.block_rows(), dest.block_cols(), outs, red.p, true);
+    return read_max(red.p, dest.get(0).precision());
+}
+
+double evaluate_block_cfl(const DeviceBackend& be, const BlockExpr& jacobian, const Tie& dest) {
+    std::vector<Out> outs;
+    for (DeviceVector* d : dest.dests) {
+        Out o;
+        o.dev = d;
+        outs.push_back(o);
+    }
+    DeviceScalar red(be.ordinal);
+    block_impl(be, jacobian, jacobian.block_rows(), jacobian.block_cols(), outs, red.p, true);
+    return read_max(red.p, dest.dests.at(0)->precision());
+}
+
+}  // namespace device
+}  // namespace fusevec

@@ -1,0 +1,427 @@
+// device_acceptance.cpp -- the reference's own API driving the B200 backend.
+//
+// Built by tests/native/Makefile against the UNMODIFIED reference (compiled
+// as namespace fvref from /root/reference; test-only linkage) plus the
+// product adapter paper_1809_09851_b200/host/fusevec_device.cpp and
+// libfvb.so.  Mirrors the reference's acceptance criteria on the hot path
+// (proj/tests/acceptance.cpp) with the device backend in place of
+// Backend::scalar_ref(), comparing bit for bit against the reference engine.
+//
+//   device_acceptance keys   -- CPU only: structural keys of the reference's
+//                               trees resolve to the fused kernels; the new
+//                               fluid objects evaluate, on the reference
+//                               engine, to the oracle composition
+//   device_acceptance gpu    -- the device path itself
+//
+// Each check prints [PASS]/[FAIL]; the exit code counts failures.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "fusevec/block.hpp"
+#include "fusevec/fluid.hpp"
+#include "fusevec/rng.hpp"
+#include "fusevec_device.hpp"
+#include "fvb.h"
+#include "fvb_oracle.h"
+
+using namespace fvref;
+namespace dev = fvref::device;
+
+namespace {
+
+int failures = 0;
+
+void check(const std::string& name, const std::function<std::string()>& fn) {
+    try {
+        std::string d = fn();
+        std::printf("[PASS] %s%s%s\n", name.c_str(), d.empty() ? "" : ": ", d.c_str());
+    } catch (const std::exception& e) {
+        std::printf("[FAIL] %s: %s\n", name.c_str(), e.what());
+        ++failures;
+    }
+    std::fflush(stdout);
+}
+
+[[noreturn]] void fail(const std::string& m) { throw std::runtime_error(m); }
+
+bool same_bits(const DenseVector& a, const DenseVector& b) {
+    return a.precision() == b.precision() && a.size() == b.size() &&
+           (a.size() == 0 || std::memcmp(a.raw(), b.raw(), a.byte_size()) == 0);
+}
+
+// random_state of proj/tests/acceptance.cpp:214-230
+std::vector<DenseVector> random_state(std::size_t dim, std::size_t n, SplitMix64& rng,
+                                      Precision prec = Precision::f64) {
+    std::vector<DenseVector> f(dim + 2, DenseVector(prec, n));
+    for (std::size_t i = 0; i < n; ++i) {
+        double rho = rng.uniform(0.5, 2.0);
+        double p = rng.uniform(0.5, 2.0);
+        double vsq = 0;
+        f[0].set(i, rho);
+        for (std::size_t j = 0; j < dim; ++j) {
+            double v = rng.uniform(-1.0, 1.0);
+            vsq += v * v;
+            f[1 + j].set(i, rho * v);
+        }
+        f[dim + 1].set(i, p / 0.4 + 0.5 * rho * vsq);
+    }
+    return f;
+}
+
+std::vector<Expr> leaves_of(const std::vector<DenseVector>& vs) {
+    std::vector<Expr> out;
+    for (const auto& v : vs) out.push_back(leaf(v));
+    return out;
+}
+
+std::string lookup_name(const std::string& key) {
+    fvb_kernel k;
+    if (fvb_lookup(key.c_str(), &k) != FVB_OK) return "";
+    return k.name;
+}
+
+std::vector<Expr> block_items(const BlockExpr& b) {
+    std::vector<Expr> items;
+    for (std::size_t r = 0; r < b.block_rows(); ++r)
+        for (std::size_t c = 0; c < b.block_cols(); ++c) items.push_back(b.item(r, c).as_expr());
+    return items;
+}
+
+std::string block_key_of(const BlockExpr& b, Precision p) {
+    auto items = block_items(b);
+    std::vector<Precision> dests(items.size(), p);
+    return dev::block_key(items, dests, b.block_rows(), b.block_cols(), nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// keys: CPU only
+// ---------------------------------------------------------------------------
+
+void run_keys() {
+    for (Precision P : {Precision::f64, Precision::f32}) {
+        const std::string sfx = P == Precision::f64 ? "_f64" : "_f32";
+        for (std::size_t d = 1; d <= 3; ++d) {
+            const std::string tag = std::to_string(d) + sfx;
+            check("keys: reference trees resolve, d" + tag, [&] {
+                SplitMix64 rng(1);
+                auto f = random_state(d, 4, rng, P);
+                StateSet u = state_conservative(EosSpec(), d, leaves_of(f));
+                struct Case {
+                    std::string want, key;
+                };
+                BlockExpr prim = convert(u, Formulation::Primitive).block();
+                std::vector<Expr> prim_items = block_items(prim);
+                prim_items.erase(prim_items.begin());  // rho passes through
+                std::vector<Expr> with_c = prim_items;
+                with_c.push_back(derived_c(u));
+                std::vector<Precision> pd(with_c.size(), P);
+                std::vector<Case> cases = {
+                    {"flux" + tag, block_key_of(inviscid_flux(u), P)},
+                    {"jacobian" + tag, block_key_of(inviscid_flux_jacobian(u), P)},
+                    {"cons2prim" + tag, dev::block_key(prim_items, std::vector<Precision>(d + 1, P),
+                                                       d + 1, 1, nullptr)},
+                    {"cons2prim_c" + tag, dev::block_key(with_c, pd, d + 2, 1, nullptr)},
+                    {"pressure" + tag, dev::structural_key(derived_p(u), P)},
+                    {"sound_speed" + tag, dev::structural_key(derived_c(u), P)},
+                    {"v_mag2" + tag, dev::structural_key(derived_v_mag2(u), P)},
+                    {"wave_speed" + tag, dev::structural_key(wave_speed(u), P)},
+                };
+                StateSet w = state_primitive(EosSpec(), d, leaves_of(f));
+                std::vector<Expr> cons_items = block_items(convert(w, Formulation::Conservative).block());
+                cons_items.erase(cons_items.begin());
+                cases.push_back({"prim2cons" + tag, dev::block_key(cons_items,
+                                                                   std::vector<Precision>(d + 1, P),
+                                                                   d + 1, 1, nullptr)});
+                for (const Case& c : cases)
+                    if (lookup_name(c.key) != c.want)
+                        fail(c.want + " not resolved from key " + c.key.substr(0, 120));
+                // a non-default gas resolves to the same kernels
+                StateSet mono = state_conservative(EosSpec(rational(5, 2), rational(3, 2)), d,
+                                                   leaves_of(f));
+                if (lookup_name(block_key_of(inviscid_flux(mono), P)) != "flux" + tag)
+                    fail("monatomic flux key not resolved");
+                return std::to_string(cases.size() + 1) + " trees";
+            });
+        }
+        check("new fluid objects on the reference engine == C oracle" + sfx, [&] {
+            // The product's derived_c / wave_speed / inviscid_flux_jacobian
+            // (fusevec_device.cpp), evaluated by the UNMODIFIED reference
+            // engine, reproduce oracle/fvb_oracle.c bit for bit.
+            for (std::size_t d = 1; d <= 3; ++d) {
+                SplitMix64 rng(77 + d);
+                const std::size_t n = 513;
+                auto f = random_state(d, n, rng, P);
+                StateSet u = state_conservative(EosSpec(), d, leaves_of(f));
+                const std::size_t w = d + 2;
+                BlockVectorGrid J(d * w, w, P, n);
+                evaluate_block(Backend::scalar_ref(), inviscid_flux_jacobian(u), J);
+                DenseVector c(P, n), lam(P, n);
+                evaluate(Backend::scalar_ref(), derived_c(u), c);
+                evaluate(Backend::scalar_ref(), wave_speed(u), lam);
+                std::vector<DenseVector> oj(d * w * w, DenseVector(P, n)), oc(d + 2, DenseVector(P, n));
+                std::vector<const void*> in;
+                for (auto& v : f) in.push_back(v.raw());
+                std::vector<void*> jo, co;
+                for (auto& v : oj) jo.push_back(v.raw());
+                for (auto& v : oc) co.push_back(v.raw());
+                fvo_gas g = fvo_default_gas();
+                if (P == Precision::f64) {
+                    fvo_jacobian_f64(g, int(d), n, (const double* const*)in.data(), (double* const*)jo.data(), nullptr);
+                    fvo_cons2prim_f64(g, int(d), n, (const double* const*)in.data(), (double* const*)co.data());
+                } else {
+                    fvo_jacobian_f32(g, int(d), n, (const float* const*)in.data(), (float* const*)jo.data(), nullptr);
+                    fvo_cons2prim_f32(g, int(d), n, (const float* const*)in.data(), (float* const*)co.data());
+                }
+                for (std::size_t i = 0; i < d * w * w; ++i)
+                    if (!same_bits(J.get(i), oj[i])) fail("jacobian item " + std::to_string(i));
+                if (!same_bits(c, oc[d + 1])) fail("sound speed");
+                double m = 0;
+                for (std::size_t i = 0; i < n; ++i) m = std::fmax(m, lam.at(i));
+                double om = P == Precision::f64 ? fvo_wave_speed_max_f64(g, int(d), n, (const double* const*)in.data())
+                                                : double(fvo_wave_speed_max_f32(g, int(d), n, (const float* const*)in.data()));
+                if (m != om) fail("wave speed max");
+            }
+            return "d = 1, 2, 3";
+        });
+        check("keys: axpy-sin and EOS" + sfx, [&] {
+            DenseVector x(P, 4), y(P, 4);
+            Expr e = constant(0.5, leaf(y)) * elem_sin(leaf(x) + leaf(y));
+            if (lookup_name(dev::structural_key(e, P)) != "axpy_sin" + sfx) fail("axpy-sin");
+            Expr et = tag(0, leaf(x));  // tags are transparent to the key
+            Expr e2 = constant(0.5, leaf(y)) * elem_sin(et + tag(1, leaf(y)));
+            if (lookup_name(dev::structural_key(e2, P)) != "axpy_sin" + sfx) fail("tagged axpy");
+            IdealGasEos gas;
+            if (lookup_name(dev::structural_key(gas.p_rhoe(leaf(x), leaf(y)), P)) != "eos_p" + sfx)
+                fail("eos_p");
+            if (lookup_name(dev::structural_key(gas.T_rhoe(leaf(x), leaf(y)), P)) != "eos_T" + sfx)
+                fail("eos_T");
+            // something with no fused kernel must not resolve
+            if (!lookup_name(dev::structural_key(elem_cos(leaf(x)), P)).empty())
+                fail("cos resolved");
+            return "";
+        });
+    }
+}
+
+// ---------------------------------------------------------------------------
+// gpu: the device path
+// ---------------------------------------------------------------------------
+
+void run_gpu() {
+    dev::DeviceBackend be;
+    Backend ref = Backend::scalar_ref();
+
+    check("criterion 6 on device: flux, d in {1,2,3} x 100 instances, n=64, bitwise", [&] {
+        SplitMix64 rng(0xF1);
+        for (std::size_t d = 1; d <= 3; ++d)
+            for (int inst = 0; inst < 100; ++inst) {
+                auto f = random_state(d, 64, rng);
+                StateSet u = state_conservative(EosSpec(), d, leaves_of(f));
+                BlockExpr flux = inviscid_flux(u);
+                BlockVectorGrid want(d + 2, d, Precision::f64, 64), got(d + 2, d, Precision::f64, 64);
+                evaluate_block(ref, flux, want);
+                dev::evaluate_block(be, flux, got);
+                for (std::size_t i = 0; i < (d + 2) * d; ++i)
+                    if (!same_bits(want.get(i), got.get(i))) fail("d=" + std::to_string(d));
+            }
+        return "";
+    });
+
+    check("criterion 6 worked instance on device: column 0 = [2,4,4,4,16]", [&] {
+        DenseVector rho({2.0}), mx({2.0}), my({4.0}), mz({4.0}), rhoE({14.0});
+        StateSet u = state_conservative(EosSpec(), 3, rho, mx, my, mz, rhoE);
+        BlockVectorGrid got(5, 3, Precision::f64, 1);
+        dev::evaluate_block(be, inviscid_flux(u), got);
+        const double want[5] = {2, 4, 4, 4, 16};
+        for (std::size_t r = 0; r < 5; ++r)
+            if (got.item(r, 0).at(0) != want[r]) fail("row " + std::to_string(r));
+        return "";
+    });
+
+    check("criterion 5 on device: round trip and p = rho R T, 100 x d, n=128", [&] {
+        SplitMix64 rng(0x7E6);
+        for (std::size_t d = 1; d <= 3; ++d)
+            for (int inst = 0; inst < 100; ++inst) {
+                auto f = random_state(d, 128, rng);
+                StateSet uc = state_conservative(EosSpec(), d, leaves_of(f));
+                // cons -> prim on the device (rho passes through)
+                std::vector<DenseVector> prim;
+                for (std::size_t i = 0; i < d + 2; ++i) prim.emplace_back(Precision::f64, 128);
+                BlockColVector pv(std::move(prim));
+                dev::evaluate_block(be, convert(uc, Formulation::Primitive).block(), pv);
+                // prim -> cons on the device
+                std::vector<Expr> pf;
+                for (std::size_t i = 0; i < d + 2; ++i) pf.push_back(leaf(pv.get(i)));
+                StateSet up = state_primitive(EosSpec(), d, pf);
+                std::vector<DenseVector> back;
+                for (std::size_t i = 0; i < d + 2; ++i) back.emplace_back(Precision::f64, 128);
+                BlockColVector bv(std::move(back));
+                dev::evaluate_block(be, convert(up, Formulation::Conservative).block(), bv);
+                for (std::size_t fi = 0; fi < d + 2; ++fi)
+                    for (std::size_t i = 0; i < 128; ++i) {
+                        double a = bv.get(fi).at(i), b = f[fi].at(i);
+                        if (std::fabs(a - b) > 1e-12 * std::fmax(std::fmax(std::fabs(a), std::fabs(b)), 1.0))
+                            fail("round trip drifted");
+                    }
+                // and the device primitive fields equal the reference's bitwise
+                StateSet w = convert(uc, Formulation::Primitive);
+                for (std::size_t fi = 1; fi < d + 2; ++fi) {
+                    DenseVector want(Precision::f64, 128);
+                    evaluate(ref, w.field(fi), want);
+                    if (!same_bits(want, pv.get(fi))) fail("primitive field differs");
+                }
+            }
+        return "";
+    });
+
+    check("fusion: zero intermediate vector allocations on the device path", [&] {
+        SplitMix64 rng(3);
+        auto f = random_state(3, 16384, rng);
+        StateSet u = state_conservative(EosSpec(), 3, leaves_of(f));
+        BlockVectorGrid grid(5, 3, Precision::f64, 16384);
+        dev::evaluate_block(be, inviscid_flux(u), grid);  // warm
+        const auto before = vector_alloc_count();
+        dev::evaluate_block(be, inviscid_flux(u), grid);
+        if (vector_alloc_count() != before) fail("DenseVector allocated");
+        return "";
+    });
+
+    check("sound speed, v_mag2, pressure, EOS and axpy-sin on device, bitwise / 4 ulp", [&] {
+        SplitMix64 rng(9);
+        auto f = random_state(3, 5000, rng);
+        StateSet u = state_conservative(EosSpec(), 3, leaves_of(f));
+        for (const Expr& e : {derived_c(u), derived_v_mag2(u), derived_p(u)}) {
+            DenseVector want(Precision::f64, 5000), got(Precision::f64, 5000);
+            evaluate(ref, e, want);
+            dev::evaluate(be, e, got);
+            if (!same_bits(want, got)) fail("derived quantity differs");
+        }
+        IdealGasEos gas;
+        DenseVector want(Precision::f64, 5000), got(Precision::f64, 5000);
+        evaluate(ref, gas.p_rhoe(leaf(f[0]), leaf(f[4])), want);
+        dev::evaluate(be, gas.p_rhoe(leaf(f[0]), leaf(f[4])), got);
+        if (!same_bits(want, got)) fail("eos p");
+        // axpy-sin in place (dest aliases leaf y), as test_backend.cpp:37-48
+        SplitMix64 r2(5);
+        DenseVector x(Precision::f64, 777), y(Precision::f64, 777);
+        for (std::size_t i = 0; i < 777; ++i) x.set(i, r2.uniform(0.25, 4.0));
+        for (std::size_t i = 0; i < 777; ++i) y.set(i, r2.uniform(0.25, 4.0));
+        DenseVector y_ref = y;
+        evaluate(ref, constant(0.5, leaf(y_ref)) * elem_sin(leaf(x) + leaf(y_ref)), y_ref);
+        dev::evaluate(be, constant(0.5, leaf(y)) * elem_sin(leaf(x) + leaf(y)), y);
+        for (std::size_t i = 0; i < 777; ++i) {
+            long long a, b;
+            double va = y.at(i), vb = y_ref.at(i);
+            std::memcpy(&a, &va, 8);
+            std::memcpy(&b, &vb, 8);
+            if (std::llabs(a - b) > 4) fail("axpy-sin beyond 4 ulp");
+        }
+        return "";
+    });
+
+    check("Jacobians + CFL on device vs the reference engine (d=3, f64 and f32)", [&] {
+        for (Precision P : {Precision::f64, Precision::f32}) {
+            SplitMix64 rng(21);
+            auto f = random_state(3, 3001, rng, P);
+            StateSet u = state_conservative(EosSpec(), 3, leaves_of(f));
+            BlockExpr J = inviscid_flux_jacobian(u);
+            BlockVectorGrid want(15, 5, P, 3001), got(15, 5, P, 3001);
+            evaluate_block(ref, J, want);
+            double lam = dev::evaluate_block_cfl(be, J, got);
+            for (std::size_t i = 0; i < 75; ++i)
+                if (!same_bits(want.get(i), got.get(i))) fail("jacobian item " + std::to_string(i));
+            DenseVector ws(P, 3001);
+            evaluate(ref, wave_speed(u), ws);
+            double m = 0;
+            for (std::size_t i = 0; i < 3001; ++i) m = std::fmax(m, ws.at(i));
+            if (lam != m) fail("fused CFL max differs from the reference max");
+            if (dev::reduce_max(be, wave_speed(u)) != m) fail("reduce_max differs");
+        }
+        return "";
+    });
+
+    check("device-resident leaves (Residency) and tie'd make_temp destinations", [&] {
+        SplitMix64 rng(33);
+        const std::size_t n = 100003;
+        auto f = random_state(3, n, rng);
+        StateSet u = state_conservative(EosSpec(), 3, leaves_of(f));
+        std::vector<dev::DeviceVector> planes;
+        dev::Residency res;
+        for (auto& v : f) {
+            planes.push_back(dev::make_temp(Precision::f64, n));
+            planes.back().upload(v);
+        }
+        for (std::size_t i = 0; i < 5; ++i) res.bind(f[i], planes[i]);
+        dev::DeviceBackend rb;
+        rb.residency = &res;
+        std::vector<dev::DeviceVector> out;
+        for (int i = 0; i < 15; ++i) out.push_back(dev::make_temp(Precision::f64, n));
+        dev::Tie t;
+        for (auto& o : out) t.dests.push_back(&o);
+        dev::evaluate_block(rb, inviscid_flux(u), t);
+        BlockVectorGrid want(5, 3, Precision::f64, n);
+        evaluate_block(ref, inviscid_flux(u), want);
+        DenseVector tmp(Precision::f64, n);
+        for (std::size_t i = 0; i < 15; ++i) {
+            out[i].download(tmp);
+            if (!same_bits(tmp, want.get(i))) fail("resident flux item " + std::to_string(i));
+        }
+        // tie() of cons->prim + c into three device temporaries, d=1
+        auto g = random_state(1, n, rng);
+        StateSet u1 = state_conservative(EosSpec(), 1, leaves_of(g));
+        auto v = dev::make_temp(Precision::f64, n), p = dev::make_temp(Precision::f64, n),
+             c = dev::make_temp(Precision::f64, n);
+        BlockExpr vpc = make_block_expr(3, 1, convert(u1, Formulation::Primitive).field(1),
+                                        derived_p(u1), derived_c(u1));
+        dev::evaluate_block(be, vpc, dev::tie(v, p, c));
+        DenseVector w(Precision::f64, n);
+        evaluate(ref, derived_c(u1), w);
+        c.download(tmp);
+        if (!same_bits(tmp, w)) fail("tied sound speed");
+        return "";
+    });
+
+    check("errors: unsupported expression, length mismatch, shape mismatch", [&] {
+        DenseVector a(Precision::f64, 10), b(Precision::f64, 11), out(Precision::f64, 10);
+        bool threw = false;
+        try {
+            dev::evaluate(be, elem_cos(leaf(a)), out);
+        } catch (const UnsupportedExpression&) {
+            threw = true;
+        }
+        if (!threw) fail("cos did not throw UnsupportedExpression");
+        threw = false;
+        try {
+            dev::evaluate(be, constant(0.5, leaf(a)) * elem_sin(leaf(a) + leaf(b)), out);
+        } catch (const LengthMismatch&) {
+            threw = true;
+        }
+        if (!threw) fail("no LengthMismatch");
+        threw = false;
+        try {
+            SplitMix64 rng(1);
+            auto f = random_state(3, 10, rng);
+            StateSet u = state_conservative(EosSpec(), 3, leaves_of(f));
+            BlockVectorGrid g(3, 3, Precision::f64, 10);
+            dev::evaluate_block(be, inviscid_flux(u), g);
+        } catch (const ShapeMismatch&) {
+            threw = true;
+        }
+        if (!threw) fail("no ShapeMismatch");
+        return "";
+    });
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    const std::string mode = argc > 1 ? argv[1] : "keys";
+    if (mode == "keys" || mode == "all") run_keys();
+    if (mode == "gpu" || mode == "all") run_gpu();
+    std::printf(failures ? "%d check(s) failed\n" : "all checks passed\n", failures);
+    return failures ? 1 : 0;
+}
