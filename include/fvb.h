@@ -121,7 +121,8 @@ FVB_API fvb_status fvb_prim2cons(const fvb_gas* gas, uint32_t dim, uint8_t prec,
                          const void* const* in, void* const* out, void* stream);
 
 /* derived_v_mag2 of a conservative state (src/fluid.cpp:243-247), the
- * paper's micro-benchmark (mx^2+my^2+mz^2)/rho^2.  out: one plane. */
+ * paper's micro-benchmark (mx^2+my^2+mz^2)/rho^2.  Reads in[0..d] (rho and
+ * the momenta; rhoE is not touched), out: one plane. */
 FVB_API fvb_status fvb_v_mag2(uint32_t dim, uint8_t prec, uint64_t n, const void* const* in,
                       void* out, void* stream);
 

@@ -156,9 +156,10 @@ struct Prim2ConsOp {
 };
 
 // derived_v_mag2, conservative (src/fluid.cpp:243-247): msq/(rho*rho).
+// Reads [rho, m_0..m_{d-1}] only (4R + 1W = 40 B/pt in 3-D fp64).
 template <class T, int D>
 struct VMag2Op {
-    static constexpr int NIN = D + 2;
+    static constexpr int NIN = D + 1;
     static constexpr int NOUT = 1;
     static constexpr bool HAS_LAMBDA = false;
     static constexpr bool ALIASED = false;

@@ -369,7 +369,8 @@ void add_fluid(std::vector<Pattern>& ps) {
     ps.back().reduce = entry_reduce<JacobianOp<T, D>, T>;
     single("pressure", derived_p(u), cn, entry<SliceOp<Cons2PrimOp<T, D>, D, 1>, T>);
     single("sound_speed", sound_speed(u), cn, entry<SliceOp<Cons2PrimOp<T, D>, D + 1, 1>, T>);
-    single("v_mag2", v_mag2(u), cn, entry<VMag2Op<T, D>, T>);
+    single("v_mag2", v_mag2(u), std::vector<std::string>(cn.begin(), cn.end() - 1),
+           entry<VMag2Op<T, D>, T>);
     single("wave_speed", wave_speed(u), cn, entry<WaveSpeedOp<T, D, 1>, T>);
     ps.back().reduce = wave_reduce<T, D>;
 }
