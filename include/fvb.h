@@ -109,6 +109,11 @@ FVB_API fvb_status fvb_axpy_sin(uint8_t prec, uint64_t n, const void* x, void* y
 FVB_API fvb_status fvb_flux(const fvb_gas* gas, uint32_t dim, uint8_t prec, uint64_t n,
                     const void* const* in, void* const* out, void* stream);
 
+/* Inviscid flux of a PRIMITIVE state [rho, v_0..v_{d-1}, p]
+ * (src/fluid.cpp:290-298): same (d+2)*d item layout as fvb_flux. */
+FVB_API fvb_status fvb_flux_prim(const fvb_gas* gas, uint32_t dim, uint8_t prec, uint64_t n,
+                                 const void* const* in, void* const* out, void* stream);
+
 /* Conservative -> primitive + EOS in one pass (src/fluid.cpp:234-258 and
  * SURVEY A.2): in: d+2 planes; out: d+2 planes [v_0..v_{d-1}, p, c].
  * rho passes through (the reference's convert reuses the density node). */

@@ -74,7 +74,7 @@ class Oracle:
             getattr(L, f"fvo_random_state_{p}").argtypes = [i32, u64, u64, u64, pp]
             getattr(L, f"fvo_make_vec_{p}").argtypes = [u64, u64, u64, dbl, dbl, vp]
             getattr(L, f"fvo_axpy_sin_{p}").argtypes = [u64, vp, vp]
-            for fn in ("flux", "cons2prim", "prim2cons"):
+            for fn in ("flux", "flux_prim", "cons2prim", "prim2cons"):
                 getattr(L, f"fvo_{fn}_{p}").argtypes = [GasC, i32, u64, pp, pp]
             getattr(L, f"fvo_v_mag2_{p}").argtypes = [i32, u64, pp, vp]
             getattr(L, f"fvo_jacobian_{p}").argtypes = [GasC, i32, u64, pp, pp, vp]
@@ -118,6 +118,9 @@ class Oracle:
 
     def flux(self, dim, state, gas=None):
         return self._block("flux", dim, state, (dim + 2) * dim, gas)
+
+    def flux_prim(self, dim, prim, gas=None):
+        return self._block("flux_prim", dim, prim, (dim + 2) * dim, gas)
 
     def cons2prim(self, dim, state, gas=None):
         return self._block("cons2prim", dim, state, dim + 2, gas)
@@ -174,6 +177,7 @@ class Reference:
         L.fvr_random_state.argtypes = [i32, i32, u64, u64, pp]
         L.fvr_axpy_sin.argtypes = [i32, u64, vp, vp, i32]
         L.fvr_flux.argtypes = [gas, i32, i32, u64, pp, pp, i32]
+        L.fvr_flux_prim.argtypes = [gas, i32, i32, u64, pp, pp, i32]
         L.fvr_cons2prim.argtypes = [gas, i32, i32, u64, pp, pp, i32]
         L.fvr_prim2cons.argtypes = [gas, i32, i32, u64, pp, pp, i32]
         L.fvr_v_mag2.argtypes = [i32, i32, u64, pp, vp, i32]
@@ -220,6 +224,9 @@ class Reference:
 
     def flux(self, dim, state, workers=0, cp=(7, 2), cv=(5, 2)):
         return self._block("flux", dim, state, (dim + 2) * dim, workers, cp, cv)
+
+    def flux_prim(self, dim, prim, workers=0, cp=(7, 2), cv=(5, 2)):
+        return self._block("flux_prim", dim, prim, (dim + 2) * dim, workers, cp, cv)
 
     def cons2prim(self, dim, state, workers=0, cp=(7, 2), cv=(5, 2)):
         return self._block("cons2prim", dim, state, dim + 2, workers, cp, cv)

@@ -225,6 +225,18 @@ int fvr_flux(const long long* gas, int dim, int prec, std::uint64_t n, const voi
     });
 }
 
+int fvr_flux_prim(const long long* gas, int dim, int prec, std::uint64_t n,
+                  const void* const* in, void* const* out, int workers) {
+    return guarded([&] {
+        auto f = upload_planes(prec_of(prec), n, std::size_t(dim) + 2, in);
+        StateSet w = state_primitive(gas_of(gas), std::size_t(dim), leaves(f));
+        BlockVectorGrid grid(std::size_t(dim) + 2, std::size_t(dim), prec_of(prec), n);
+        evaluate_block(backend_of(workers), inviscid_flux(w), grid);
+        for (std::size_t i = 0; i < std::size_t(dim + 2) * std::size_t(dim); ++i)
+            download(grid.get(i), out[i]);
+    });
+}
+
 int fvr_cons2prim(const long long* gas, int dim, int prec, std::uint64_t n,
                   const void* const* in, void* const* out, int workers) {
     return guarded([&] {

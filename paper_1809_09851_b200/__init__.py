@@ -24,6 +24,7 @@ from .device import (  # noqa: F401
     cons2prim,
     eos,
     flux,
+    flux_prim,
     jacobian,
     lookup,
     patterns,

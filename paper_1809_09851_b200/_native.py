@@ -22,6 +22,7 @@ EXPORTED = (
     "fvb_build_info",
     "fvb_axpy_sin",
     "fvb_flux",
+    "fvb_flux_prim",
     "fvb_cons2prim",
     "fvb_prim2cons",
     "fvb_v_mag2",
@@ -137,6 +138,7 @@ def _declare(L):
         "fvb_build_info": (ctypes.c_char_p, []),
         "fvb_axpy_sin": (i32, [u8, u64, vp, vp, vp]),
         "fvb_flux": (i32, [gas, u32, u8, u64, pp, pp, vp]),
+        "fvb_flux_prim": (i32, [gas, u32, u8, u64, pp, pp, vp]),
         "fvb_cons2prim": (i32, [gas, u32, u8, u64, pp, pp, vp]),
         "fvb_prim2cons": (i32, [gas, u32, u8, u64, pp, pp, vp]),
         "fvb_v_mag2": (i32, [u32, u8, u64, pp, vp, vp]),

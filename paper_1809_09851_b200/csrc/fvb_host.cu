@@ -14,6 +14,8 @@
 #include <algorithm>
 #include <cstring>
 #include <new>
+#include <thread>
+#include <vector>
 
 #include "fvb.h"
 #include "fvb_launch.cuh"
@@ -69,7 +71,38 @@ uint64_t chunk_for(const fvb_ctx* ctx, size_t bytes_per_point, uint64_t n) {
     return std::min<uint64_t>(c, std::max<uint64_t>(n, 1));
 }
 
-template <class Op, class T, bool RED, bool TUNE>
+// Host threads copying pass-through items: output j < PASS is bit-for-bit
+// input plane 1 + j (the flux's row 0 is the momentum fields themselves,
+// include/fusevec/fluid.hpp:168-169).  The host already holds those bytes,
+// so they are copied host-side, concurrently with the device pipeline,
+// instead of crossing PCIe twice.  Joined on every exit path.
+struct PassThrough {
+    std::vector<std::thread> workers;
+    PassThrough(const void* const* in, void* const* out, int pass, size_t bytes) {
+        if (pass <= 0 || bytes == 0) return;
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const unsigned nt = std::min(8u, std::max(1u, hw / 2));
+        const size_t total = size_t(pass) * bytes;
+        const size_t per = (total + nt - 1) / nt;
+        for (unsigned t = 0; t < nt; ++t) {
+            workers.emplace_back([=] {
+                size_t lo = size_t(t) * per, hi = std::min(total, lo + per);
+                while (lo < hi) {
+                    const size_t plane = lo / bytes, at = lo % bytes;
+                    const size_t len = std::min(hi - lo, bytes - at);
+                    std::memcpy(static_cast<char*>(out[plane]) + at,
+                                static_cast<const char*>(in[1 + plane]) + at, len);
+                    lo += len;
+                }
+            });
+        }
+    }
+    ~PassThrough() {
+        for (auto& w : workers) w.join();
+    }
+};
+
+template <class Op, class T, bool RED, bool TUNE, int PASS = 0>
 fvb_status pipeline(fvb_ctx* ctx, const void* const* in, void* const* out, uint64_t n,
                     const Consts<T>& k, double* lambda_max) {
     constexpr int NIN = Op::NIN, NOUT = Op::NOUT;
@@ -94,6 +127,7 @@ fvb_status pipeline(fvb_ctx* ctx, const void* const* in, void* const* out, uint6
     const uint64_t chunk = chunk_for(ctx, sizeof(T) * (NIN + NOUT), n);
     if (fvb_status st = ensure_slots(ctx, size_t(chunk) * sizeof(T) * (NIN + NOUT))) return st;
 
+    PassThrough pass(in, out, PASS, size_t(n) * sizeof(T));
     const uint64_t nchunks = (n + chunk - 1) / chunk;
     for (uint64_t c = 0; c < nchunks; ++c) {
         const int slot = int(c % fvb_ctx::kSlots);
@@ -115,7 +149,7 @@ fvb_status pipeline(fvb_ctx* ctx, const void* const* in, void* const* out, uint6
         fvb_status st = launch_op<Op, T, RED, TUNE>(din, dout, cnt, k,
                                                     static_cast<Bu*>(ctx->red), s);
         if (st) return st;
-        for (int j = 0; j < NOUT; ++j) {
+        for (int j = PASS; j < NOUT; ++j) {
             const cudaError_t e = cudaMemcpyAsync(static_cast<T*>(out[j]) + off, dout[j], bytes,
                                                   cudaMemcpyDeviceToHost, s);
             if (e != cudaSuccess) return cuda_fail(e, "device->host copy");
@@ -136,14 +170,22 @@ fvb_status pipeline(fvb_ctx* ctx, const void* const* in, void* const* out, uint6
     return FVB_OK;
 }
 
-template <template <class, int> class OpT, bool RED, class T, bool TUNE3 = false>
+// PASS_DIM: the first d outputs are pass-through copies of inputs 1..d.
+template <template <class, int> class OpT, bool RED, class T, bool TUNE3 = false,
+          bool PASS_DIM = false>
 fvb_status pipeline_dim(fvb_ctx* ctx, const fvb_gas* gas, uint32_t dim, const void* const* in,
                         void* const* out, uint64_t n, double* lambda_max) {
     const auto k = make_consts<T>(gas);
     switch (dim) {
-        case 1: return pipeline<OpT<T, 1>, T, RED, false>(ctx, in, out, n, k, lambda_max);
-        case 2: return pipeline<OpT<T, 2>, T, RED, false>(ctx, in, out, n, k, lambda_max);
-        default: return pipeline<OpT<T, 3>, T, RED, TUNE3>(ctx, in, out, n, k, lambda_max);
+        case 1:
+            return pipeline<OpT<T, 1>, T, RED, false, PASS_DIM ? 1 : 0>(ctx, in, out, n, k,
+                                                                        lambda_max);
+        case 2:
+            return pipeline<OpT<T, 2>, T, RED, false, PASS_DIM ? 2 : 0>(ctx, in, out, n, k,
+                                                                        lambda_max);
+        default:
+            return pipeline<OpT<T, 3>, T, RED, TUNE3, PASS_DIM ? 3 : 0>(ctx, in, out, n, k,
+                                                                        lambda_max);
     }
 }
 
@@ -205,8 +247,8 @@ fvb_status fvb_flux_host(fvb_ctx* ctx, const fvb_gas* gas, uint32_t dim, uint8_t
                          uint64_t n, const void* const* in, void* const* out) {
     if (fvb_status st = check(ctx, gas, dim, prec)) return st;
     if (prec == FVB_F64)
-        return pipeline_dim<FluxOp, false, double, true>(ctx, gas, dim, in, out, n, nullptr);
-    return pipeline_dim<FluxOp, false, float, true>(ctx, gas, dim, in, out, n, nullptr);
+        return pipeline_dim<FluxOp, false, double, true, true>(ctx, gas, dim, in, out, n, nullptr);
+    return pipeline_dim<FluxOp, false, float, true, true>(ctx, gas, dim, in, out, n, nullptr);
 }
 
 fvb_status fvb_jacobian_host(fvb_ctx* ctx, const fvb_gas* gas, uint32_t dim, uint8_t prec,

@@ -96,6 +96,45 @@ struct FluxOp {
 };
 
 // ---------------------------------------------------------------------------
+// inviscid_flux of a PRIMITIVE state [rho, v.., p] (src/fluid.cpp:290-298):
+//   rho_v_j = rho*v_j;  rhoE = p/gm1 + 0.5*(rho*vsq);
+//   F(0,j) = rho_v_j;  F(1+i,j) = rho_v_i*v_j [+ p iff i==j];
+//   F(d+1,j) = v_j*(rhoE + p).
+// ---------------------------------------------------------------------------
+template <class T, int D>
+struct FluxPrimOp {
+    static constexpr int NIN = D + 2;
+    static constexpr int NOUT = (D + 2) * D;
+    static constexpr bool HAS_LAMBDA = false;
+    static constexpr bool ALIASED = false;
+    struct State {
+        T rv[D], v[D], p, rho_E;
+    };
+    __device__ __forceinline__ static State prepare(const T (&in)[NIN], const Consts<T>& k) {
+        State s;
+        const T rho = in[0];
+#pragma unroll
+        for (int j = 0; j < D; ++j) s.v[j] = in[1 + j];
+        s.p = in[D + 1];
+#pragma unroll
+        for (int j = 0; j < D; ++j) s.rv[j] = rho * s.v[j];
+        s.rho_E = s.p / k.gm1 + k.half * (rho * sum_sq<D>(s.v));
+        return s;
+    }
+    __device__ __forceinline__ static T out(const State& s, int item, const Consts<T>&) {
+        const int r = item / D, c = item % D;
+        if (r == 0) return s.rv[c];
+        if (r <= D) {
+            T f = s.rv[r - 1] * s.v[c];
+            if (r - 1 == c) f = f + s.p;
+            return f;
+        }
+        return s.v[c] * (s.rho_E + s.p);
+    }
+    __device__ __forceinline__ static T lambda(const State&, const Consts<T>&) { return T(0); }
+};
+
+// ---------------------------------------------------------------------------
 // convert(u, Primitive) fields 1..d+1 (src/fluid.cpp:249-258) + sound speed:
 //   out = [m_0/rho, ..., m_{d-1}/rho, p, sqrt((gamma*p)/rho)]
 // ---------------------------------------------------------------------------

@@ -205,6 +205,25 @@ std::vector<N> cons_items(int d) {
     return items;
 }
 
+// inviscid_flux, primitive (fluid.cpp:290-298)
+std::vector<N> flux_prim_items(int d) {
+    N rho = leaf("rho"), v[3], rv[3], p = leaf("p");
+    for (int j = 0; j < d; ++j) v[j] = leaf("v" + std::to_string(j));
+    for (int j = 0; j < d; ++j) rv[j] = mul(rho, v[j]);
+    N vsq = sum_sq(v, d);
+    N rho_E = add(dvd(p, cst("gm1")), mul(cst("half"), mul(rho, vsq)));
+    std::vector<N> items;
+    for (int j = 0; j < d; ++j) items.push_back(rv[j]);
+    for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j) {
+            N f = mul(rv[i], v[j]);
+            if (i == j) f = add(f, p);
+            items.push_back(f);
+        }
+    for (int j = 0; j < d; ++j) items.push_back(mul(v[j], add(rho_E, p)));
+    return items;
+}
+
 // Flux Jacobians, SURVEY A.3, items [k][r][c]
 std::vector<N> jacobian_items(const Cons& u) {
     const int d = u.d, w = d + 2;
@@ -365,6 +384,7 @@ void add_fluid(std::vector<Pattern>& ps) {
           entry<SliceOp<Cons2PrimOp<T, D>, 0, D + 1>, T>);
     block("cons2prim_c", D + 2, 1, prim_items(u, true), cn, entry<Cons2PrimOp<T, D>, T>);
     block("prim2cons", D + 1, 1, cons_items(D), prim_names(D), entry<Prim2ConsOp<T, D>, T>);
+    block("flux_prim", D + 2, D, flux_prim_items(D), prim_names(D), entry<FluxPrimOp<T, D>, T>);
     block("jacobian", D * (D + 2), D + 2, jacobian_items(u), cn, entry<JacobianOp<T, D>, T>);
     ps.back().reduce = entry_reduce<JacobianOp<T, D>, T>;
     single("pressure", derived_p(u), cn, entry<SliceOp<Cons2PrimOp<T, D>, D, 1>, T>);

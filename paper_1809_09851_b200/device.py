@@ -119,6 +119,17 @@ def flux(state: Sequence[torch.Tensor], dim: int, out=None, gas: Optional[Gas] =
     return out
 
 
+def flux_prim(prim, dim, out=None, gas=None, stream=None):
+    """inviscid_flux of a primitive state [rho, v.., p] (fluid.cpp:290-298)."""
+    ins, n, prec = _state(prim, dim)
+    if out is None:
+        out = _alloc((dim + 2) * dim, n, prec, prim[0].device)
+    outs, _, _ = _planes(out, "flux_prim out", n, prec)
+    N.check(N.lib().fvb_flux_prim(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins),
+                                  N.ptr_array(outs), _stream(stream)))
+    return out
+
+
 def cons2prim(state, dim, out=None, gas=None, stream=None):
     """[v_0..v_{d-1}, p, c] of a conservative state."""
     ins, n, prec = _state(state, dim)

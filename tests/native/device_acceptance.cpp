@@ -136,6 +136,7 @@ void run_keys() {
                 cases.push_back({"prim2cons" + tag, dev::block_key(cons_items,
                                                                    std::vector<Precision>(d + 1, P),
                                                                    d + 1, 1, nullptr)});
+                cases.push_back({"flux_prim" + tag, block_key_of(inviscid_flux(w), P)});
                 for (const Case& c : cases)
                     if (lookup_name(c.key) != c.want)
                         fail(c.want + " not resolved from key " + c.key.substr(0, 120));

@@ -87,7 +87,7 @@ def test_patterns_cover_every_block():
     names = {n for n, _ in fvb.patterns()}
     for d in (1, 2, 3):
         for p in ("f32", "f64"):
-            for block in ("flux", "cons2prim", "cons2prim_c", "prim2cons", "jacobian",
+            for block in ("flux", "flux_prim", "cons2prim", "cons2prim_c", "prim2cons", "jacobian",
                           "pressure", "sound_speed", "v_mag2", "wave_speed"):
                 assert f"{block}{d}_{p}" in names
     for p in ("f32", "f64"):

@@ -24,7 +24,7 @@ def run(mode):
 
 def test_reference_trees_resolve_to_fused_kernels():
     out = run("keys")
-    assert out.count("[PASS]") == 10
+    assert out.count("[PASS]") == 10 and "11 trees" in out
 
 
 @pytest.mark.gpu

@@ -75,6 +75,7 @@ def test_fluid_blocks_bitwise_vs_reference(orc, ref, prec, dim, n):
     c = orc.cons2prim(dim, s)
     prim = [s[0]] + c[:dim] + [c[dim]]
     assert all(bits_equal(x, y) for x, y in zip(orc.prim2cons(dim, prim), ref.prim2cons(dim, prim)))
+    assert all(bits_equal(x, y) for x, y in zip(orc.flux_prim(dim, prim), ref.flux_prim(dim, prim)))
     j, lam = orc.jacobian(dim, s)
     j2, lam2 = ref.jacobian(dim, s)
     assert all(bits_equal(x, y) for x, y in zip(j, j2))

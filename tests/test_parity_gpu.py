@@ -87,6 +87,8 @@ def test_fluid_blocks_bitwise(cuda, orc, prec, dim):
         prim_np = [s_np[0]] + c[:dim] + [c[dim]]
         assert all_same(to_host(fvb.prim2cons(to_dev(prim_np, cuda), dim)),
                         orc.prim2cons(dim, prim_np)), ("prim2cons", n)
+        assert all_same(to_host(fvb.flux_prim(to_dev(prim_np, cuda), dim)),
+                        orc.flux_prim(dim, prim_np)), ("flux_prim", n)
         assert same_bits(to_host([fvb.v_mag2(s, dim)])[0], orc.v_mag2(dim, s_np))
         j, lam = fvb.jacobian(s, dim)
         j_np, lam_np = orc.jacobian(dim, s_np)
