@@ -195,17 +195,36 @@ struct fvb_kernel {
     uint8_t dim;         /* spatial dimension of a fluid block (0 otherwise)  */
     int8_t in_slot[8];   /* canonical input i is args[n_outputs + in_slot[i]] */
     double consts[8];    /* captured constants, named per kernel  */
-    char name[48];       /* e.g. "flux3_f64"                                  */
+    char name[48];       /* e.g. "flux3_f64", or "gen:<hash>" when lowered    */
+    const void* impl;    /* opaque: the NVRTC-lowered kernel, else NULL       */
 };
 
 /* Resolve a structural key.  Single expressions use the reference's own
  * key grammar verbatim (dest precision char + key_node of the tree,
  * src/backend_jit.cpp:112-155, 319-322); fused block expressions use
  * "G<rows>x<cols>:" followed by one such key per item with leaf slots
- * numbered across the whole block.  Constants in the key
- * are captured into out->consts.  FVB_EUNSUPPORTED when no hand-written
- * kernel implements the tree. */
+ * numbered across the whole block.
+ *
+ * A key matching a hand-written fused kernel returns it, with the key's
+ * constants captured into out->consts.  Any other well-formed key is lowered
+ * -- the B200 counterpart of the reference's runtime JIT
+ * (src/backend_jit.cpp:179-335) -- into one CUDA kernel: every item of the
+ * block computed per element with common subexpressions shared across
+ * items, each node in its own precision with operands converted first and
+ * constants as exact hex literals (the reference's emit / emit_as rules),
+ * compiled by NVRTC for sm_100a with --fmad=false and cached per key for
+ * the process lifetime.  FVB_EUNSUPPORTED for a malformed key, a
+ * non-finite constant or when NVRTC is unavailable; FVB_ECUDA when the
+ * compiled kernel cannot be loaded (no device). */
 FVB_API fvb_status fvb_lookup(const char* key, fvb_kernel* out);
+
+/* The CUDA source fvb_lookup would compile for `key` (NUL-terminated into
+ * buf when it fits; *len receives the full length).  Pure host code. */
+FVB_API fvb_status fvb_emit_source(const char* key, char* buf, size_t cap, size_t* len);
+
+/* Compile `key`'s lowered kernel with NVRTC without loading it (no GPU
+ * needed); *cubin_bytes receives the sm_100a image size. */
+FVB_API fvb_status fvb_nvrtc_compile(const char* key, size_t* cubin_bytes);
 
 /* Number of registered patterns and the i-th pattern (wildcards "C?*;"
  * stand for captured constants), for diagnostics and tests. */

@@ -22,11 +22,13 @@ from .device import (  # noqa: F401
     HostContext,
     axpy_sin,
     cons2prim,
+    emit_source,
     eos,
     flux,
     flux_prim,
     jacobian,
     lookup,
+    nvrtc_compile,
     patterns,
     prim2cons,
     synth_state,

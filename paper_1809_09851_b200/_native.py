@@ -32,6 +32,8 @@ EXPORTED = (
     "fvb_synth_state",
     "fvb_synth_uniform",
     "fvb_lookup",
+    "fvb_emit_source",
+    "fvb_nvrtc_compile",
     "fvb_pattern_count",
     "fvb_pattern",
     "fvb_ctx_create",
@@ -116,6 +118,7 @@ KernelStruct._fields_ = [
     ("in_slot", ctypes.c_int8 * 8),
     ("consts", ctypes.c_double * 8),
     ("name", ctypes.c_char * 48),
+    ("impl", ctypes.c_void_p),
 ]
 
 
@@ -149,6 +152,9 @@ def _declare(L):
         "fvb_synth_uniform": (i32, [u8, u64, u64, u64, ctypes.c_double, ctypes.c_double, vp,
                                     vp]),
         "fvb_lookup": (i32, [ctypes.c_char_p, ctypes.POINTER(KernelStruct)]),
+        "fvb_emit_source": (i32, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t,
+                                  ctypes.POINTER(ctypes.c_size_t)]),
+        "fvb_nvrtc_compile": (i32, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)]),
         "fvb_pattern_count": (u32, []),
         "fvb_pattern": (ctypes.c_char_p, [u32, ctypes.POINTER(ctypes.c_char_p)]),
         "fvb_ctx_create": (i32, [i32, u64, ctypes.POINTER(vp)]),

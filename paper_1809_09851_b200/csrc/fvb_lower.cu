@@ -1,0 +1,500 @@
+// fvb_lower.cu -- general lowering: any structural key -> one CUDA kernel.
+//
+// The B200 counterpart of the reference's runtime JIT
+// (proj/src/backend_jit.cpp): there a tree becomes C source, `cc -O3`, and
+// dlopen; here the structural key -- which already encodes the whole tree:
+// ops, per-node precisions, leaf slots and the exact constant bits
+// (key_node, backend_jit.cpp:112-155) -- is parsed back into a DAG and
+// emitted as CUDA source, compiled by NVRTC for sm_100a with --fmad=false
+// (the reference's -ffp-contract=off), and loaded with the runtime library
+// API.  It is cached per key for the process lifetime, like the JIT cache
+// (backend_jit.cpp:240-253, 314-335).
+//
+// Semantics follow the reference's emit / emit_as (backend_jit.cpp:179-205):
+// every node computes in its own precision, operands are converted to it
+// first, constants are exact hex literals of the narrowed value, and the
+// destination store rounds once.  Across the items of a block every
+// distinct subtree is computed once (common-subexpression sharing; bitwise
+// neutral).  Each thread loads all leaves of an element before storing any
+// output, so a destination may alias a leaf as in the reference
+// (backend.hpp:44-46).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fvb.h"
+#include "fvb_launch.cuh"
+#include "fvb_lower.h"
+
+namespace fvb {
+namespace {
+
+constexpr int kMaxArgs = 128;
+constexpr int kThreads = 256;
+constexpr int kPerThread = 4;
+
+// ---- the key's DAG ---------------------------------------------------------
+
+struct KNode {
+    char kind;  // 'L', 'C', 'U', 'B'
+    char prec;  // 's' or 'd'
+    int op = 0;
+    int slot = -1;
+    double value = 0;
+    int l = -1, r = -1;  // child node indices
+    std::string canon;   // exact key text of the subtree (CSE identity)
+};
+
+struct KDag {
+    std::vector<KNode> nodes;
+    std::vector<int> roots;        // one per item
+    std::vector<char> dest_prec;   // one per item
+    std::map<int, char> slot_prec;
+    int rows = 1, cols = 1;
+    bool block = false;
+};
+
+class Parser {
+  public:
+    Parser(const char* s, KDag& d) : s_(s), d_(d) {}
+
+    bool parse() {
+        if (*s_ == 'G') {
+            ++s_;
+            d_.block = true;
+            if (!number(&d_.rows) || *s_++ != 'x' || !number(&d_.cols) || *s_++ != ':')
+                return false;
+            for (;;) {
+                if (!item()) return false;
+                if (*s_ == '|') {
+                    ++s_;
+                    continue;
+                }
+                break;
+            }
+            return *s_ == '\0' && int(d_.roots.size()) == d_.rows * d_.cols;
+        }
+        return item() && *s_ == '\0';
+    }
+
+  private:
+    const char* s_;
+    KDag& d_;
+    std::map<std::string, int> seen_;
+
+    bool number(int* out) {
+        if (*s_ < '0' || *s_ > '9') return false;
+        long v = 0;
+        while (*s_ >= '0' && *s_ <= '9') {
+            v = v * 10 + (*s_++ - '0');
+            if (v > 1 << 20) return false;
+        }
+        *out = int(v);
+        return true;
+    }
+
+    bool prec(char* p) {
+        if (*s_ != 's' && *s_ != 'd') return false;
+        *p = *s_++;
+        return true;
+    }
+
+    bool item() {
+        char p;
+        if (!prec(&p)) return false;
+        int root;
+        if (!node(&root)) return false;
+        d_.roots.push_back(root);
+        d_.dest_prec.push_back(p);
+        return true;
+    }
+
+    bool node(int* out) {
+        const char* start = s_;
+        KNode n;
+        n.kind = *s_++;
+        switch (n.kind) {
+            case 'L': {
+                if (!prec(&n.prec) || !number(&n.slot) || *s_++ != ';') return false;
+                auto it = d_.slot_prec.find(n.slot);
+                if (it != d_.slot_prec.end() && it->second != n.prec) return false;
+                d_.slot_prec[n.slot] = n.prec;
+                break;
+            }
+            case 'C': {
+                if (!prec(&n.prec)) return false;
+                unsigned long long bits = 0;
+                for (int h = 0; h < 16; ++h) {
+                    const char c = *s_++;
+                    int v;
+                    if (c >= '0' && c <= '9') v = c - '0';
+                    else if (c >= 'a' && c <= 'f') v = c - 'a' + 10;
+                    else return false;
+                    bits = (bits << 4) | unsigned(v);
+                }
+                if (*s_++ != ';') return false;
+                std::memcpy(&n.value, &bits, sizeof bits);
+                if (!std::isfinite(n.value)) return false;  // the JIT refuses these too
+                break;
+            }
+            case 'U':
+            case 'B': {
+                if (!number(&n.op)) return false;
+                if (n.kind == 'U' ? n.op > 20 : n.op > 7) return false;
+                if (!prec(&n.prec) || *s_++ != '(') return false;
+                if (!node(&n.l)) return false;
+                if (n.kind == 'B') {
+                    if (*s_++ != ',') return false;
+                    if (!node(&n.r)) return false;
+                }
+                if (*s_++ != ')') return false;
+                break;
+            }
+            default:
+                return false;
+        }
+        n.canon.assign(start, s_);
+        auto it = seen_.find(n.canon);
+        if (it != seen_.end()) {
+            *out = it->second;  // shared subtree: one node
+            return true;
+        }
+        d_.nodes.push_back(std::move(n));
+        *out = int(d_.nodes.size() - 1);
+        seen_[d_.nodes.back().canon] = *out;
+        return true;
+    }
+};
+
+// ---- emission -------------------------------------------------------------------
+
+const char* ctype(char p) { return p == 's' ? "float" : "double"; }
+
+const char* unary_fn(int op) {
+    static const char* names[] = {nullptr, "fabs", "sin",  "cos",   "tan",   "asin", "acos",
+                                  "atan",  "sinh", "cosh", "tanh",  "exp",   "log",  "log2",
+                                  "log10", "sqrt", "cbrt", "ceil",  "floor", "round", "erf"};
+    return names[op];
+}
+
+const char* binary_infix(int op) {
+    switch (op) {
+        case 0: return "+";
+        case 1: return "-";
+        case 2: return "*";
+        case 3: return "/";
+        default: return nullptr;
+    }
+}
+
+const char* binary_fn(int op) {
+    switch (op) {
+        case 4: return "pow";
+        case 5: return "fmin";
+        case 6: return "fmax";
+        default: return "atan2";
+    }
+}
+
+std::string literal(double v, char p) {
+    char buf[64];
+    if (p == 's')
+        std::snprintf(buf, sizeof buf, "(%af)", v);
+    else
+        std::snprintf(buf, sizeof buf, "(%a)", v);
+    return buf;
+}
+
+struct Emitter {
+    const KDag& d;
+    std::vector<std::string> name;  // per node: expression to use
+    std::string body;
+    int temps = 0;
+
+    explicit Emitter(const KDag& dag) : d(dag), name(dag.nodes.size()) {}
+
+    std::string as(char want, int idx) {
+        const std::string& e = get(idx);
+        if (d.nodes[idx].prec == want) return e;
+        return std::string("(") + ctype(want) + ")(" + e + ")";
+    }
+
+    const std::string& get(int idx) {
+        if (!name[idx].empty()) return name[idx];
+        const KNode& n = d.nodes[idx];
+        std::string expr;
+        switch (n.kind) {
+            case 'L':
+                name[idx] = "l" + std::to_string(n.slot);
+                return name[idx];
+            case 'C':
+                name[idx] = literal(n.value, n.prec);
+                return name[idx];
+            case 'U': {
+                const std::string c = as(n.prec, n.l);
+                if (n.op == 0) {
+                    expr = "(-(" + c + "))";
+                } else {
+                    std::string fn = unary_fn(n.op);
+                    if (n.prec == 's') fn += 'f';
+                    expr = fn + "(" + c + ")";
+                }
+                break;
+            }
+            default: {
+                const std::string a = as(n.prec, n.l);
+                const std::string b = as(n.prec, n.r);
+                if (const char* op = binary_infix(n.op)) {
+                    expr = "(" + a + " " + op + " " + b + ")";
+                } else {
+                    std::string fn = binary_fn(n.op);
+                    if (n.prec == 's') fn += 'f';
+                    expr = fn + "(" + a + ", " + b + ")";
+                }
+                break;
+            }
+        }
+        const std::string t = "t" + std::to_string(temps++);
+        body += std::string("            const ") + ctype(n.prec) + " " + t + " = " + expr + ";\n";
+        name[idx] = t;
+        return name[idx];
+    }
+};
+
+bool emit(const char* key, std::string* src, KDag* dag_out) {
+    KDag d;
+    Parser p(key, d);
+    if (!p.parse()) return false;
+    const int nout = int(d.roots.size());
+    const int nin = d.slot_prec.empty() ? 0 : d.slot_prec.rbegin()->first + 1;
+    if (int(d.slot_prec.size()) != nin) return false;  // slots must be dense 0..nin-1
+    if (nout + nin > kMaxArgs) return false;
+    Emitter e(d);
+    std::vector<std::string> roots;
+    for (int r : d.roots) roots.push_back(e.as(d.dest_prec[roots.size()], r));
+    std::string s;
+    s += "// lowered by libfvb from a structural key (proj/src/backend_jit.cpp grammar)\n";
+    s += "typedef unsigned long long fvb_u64;\n";
+    s += "struct FvbArgs { void* p[" + std::to_string(kMaxArgs) + "]; };\n";
+    s += "extern \"C\" __global__ void __launch_bounds__(" + std::to_string(kThreads) +
+         ") fvb_gen(const FvbArgs a, const fvb_u64 n)\n{\n";
+    for (int j = 0; j < nout; ++j)
+        s += std::string("    ") + ctype(d.dest_prec[j]) + "* o" + std::to_string(j) + " = (" +
+             ctype(d.dest_prec[j]) + "*)a.p[" + std::to_string(j) + "];\n";
+    for (int i = 0; i < nin; ++i) {
+        const char* t = ctype(d.slot_prec.at(i));
+        s += std::string("    const ") + t + "* q" + std::to_string(i) + " = (const " + t +
+             "*)a.p[" + std::to_string(nout + i) + "];\n";
+    }
+    s += "    const fvb_u64 base = (fvb_u64)blockIdx.x * " + std::to_string(kThreads * kPerThread) +
+         "ull + threadIdx.x;\n";
+    s += "#pragma unroll\n    for (int u = 0; u < " + std::to_string(kPerThread) + "; ++u) {\n";
+    s += "        const fvb_u64 i = base + (fvb_u64)u * " + std::to_string(kThreads) + "ull;\n";
+    s += "        if (i < n) {\n";
+    for (int i = 0; i < nin; ++i)
+        s += std::string("            const ") + ctype(d.slot_prec.at(i)) + " l" + std::to_string(i) +
+             " = q" + std::to_string(i) + "[i];\n";
+    s += e.body;
+    for (int j = 0; j < nout; ++j)
+        s += "            o" + std::to_string(j) + "[i] = " + roots[j] + ";\n";
+    s += "        }\n    }\n}\n";
+    *src = s;
+    if (dag_out) *dag_out = std::move(d);
+    return true;
+}
+
+// ---- NVRTC, loaded at run time ---------------------------------------------------
+
+struct Nvrtc {
+    bool ok = false;
+    std::string why;
+    decltype(&nvrtcCreateProgram) create = nullptr;
+    decltype(&nvrtcCompileProgram) compile = nullptr;
+    decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
+    decltype(&nvrtcGetProgramLog) log = nullptr;
+    decltype(&nvrtcGetCUBINSize) cubin_size = nullptr;
+    decltype(&nvrtcGetCUBIN) cubin = nullptr;
+    decltype(&nvrtcDestroyProgram) destroy = nullptr;
+};
+
+const Nvrtc& nvrtc() {
+    static const Nvrtc lib = [] {
+        Nvrtc n;
+        void* h = nullptr;
+        for (const char* name : {"libnvrtc.so.12", "libnvrtc.so",
+                                 "/usr/local/cuda/lib64/libnvrtc.so.12"}) {
+            h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
+            if (h) break;
+        }
+        if (!h) {
+            n.why = "libnvrtc.so.12 not found";
+            return n;
+        }
+        n.create = reinterpret_cast<decltype(n.create)>(dlsym(h, "nvrtcCreateProgram"));
+        n.compile = reinterpret_cast<decltype(n.compile)>(dlsym(h, "nvrtcCompileProgram"));
+        n.log_size = reinterpret_cast<decltype(n.log_size)>(dlsym(h, "nvrtcGetProgramLogSize"));
+        n.log = reinterpret_cast<decltype(n.log)>(dlsym(h, "nvrtcGetProgramLog"));
+        n.cubin_size = reinterpret_cast<decltype(n.cubin_size)>(dlsym(h, "nvrtcGetCUBINSize"));
+        n.cubin = reinterpret_cast<decltype(n.cubin)>(dlsym(h, "nvrtcGetCUBIN"));
+        n.destroy = reinterpret_cast<decltype(n.destroy)>(dlsym(h, "nvrtcDestroyProgram"));
+        n.ok = n.create && n.compile && n.log_size && n.log && n.cubin_size && n.cubin && n.destroy;
+        if (!n.ok) n.why = "libnvrtc lacks a required symbol";
+        return n;
+    }();
+    return lib;
+}
+
+fvb_status compile(const std::string& src, std::vector<char>* image) {
+    const Nvrtc& nv = nvrtc();
+    if (!nv.ok) return fail(FVB_EUNSUPPORTED, "general lowering unavailable: " + nv.why);
+    nvrtcProgram prog;
+    if (nv.create(&prog, src.c_str(), "fvb_gen.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+        return fail(FVB_EUNSUPPORTED, "nvrtcCreateProgram failed");
+    const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--prec-div=true",
+                          "--prec-sqrt=true", "--ftz=false", "--std=c++17", "-default-device"};
+    const nvrtcResult rc = nv.compile(prog, int(sizeof(opts) / sizeof(opts[0])), opts);
+    if (rc != NVRTC_SUCCESS) {
+        size_t n = 0;
+        nv.log_size(prog, &n);
+        std::string log(n, '\0');
+        if (n) nv.log(prog, &log[0]);
+        nv.destroy(&prog);
+        return fail(FVB_EUNSUPPORTED, "NVRTC compile failed: " + log.substr(0, 400));
+    }
+    size_t bytes = 0;
+    nv.cubin_size(prog, &bytes);
+    image->resize(bytes);
+    nv.cubin(prog, image->data());
+    nv.destroy(&prog);
+    return FVB_OK;
+}
+
+// ---- the per-key cache and the launch entry -----------------------------------
+
+struct Gen {
+    std::string key;
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t kernel = nullptr;
+    std::vector<char> arg_prec;  // 's'/'d' per argument slot (outputs, then leaves)
+    uint32_t nout = 0, nin = 0;
+};
+
+std::mutex g_mu;
+std::map<std::string, std::unique_ptr<Gen>>& cache() {
+    static std::map<std::string, std::unique_ptr<Gen>> c;
+    return c;
+}
+
+struct LaunchArgs {
+    void* p[kMaxArgs];
+};
+
+fvb_status gen_entry(const fvb_kernel* k, uint64_t begin, uint64_t end, void* const* args,
+                     void* stream) {
+    if (!k || !k->impl || !args) return fail(FVB_EARG, "NULL kernel or argument block");
+    if (end < begin) return fail(FVB_EARG, "end < begin");
+    const Gen* g = static_cast<const Gen*>(k->impl);
+    uint64_t n = end - begin;
+    if (n == 0) return FVB_OK;
+    LaunchArgs la;
+    std::memset(&la, 0, sizeof la);
+    for (uint32_t i = 0; i < g->nout + g->nin; ++i) {
+        if (!args[i]) return fail(FVB_EARG, "NULL argument slot");
+        const size_t w = g->arg_prec[i] == 's' ? sizeof(float) : sizeof(double);
+        if (reinterpret_cast<uintptr_t>(args[i]) % w)
+            return fail(FVB_EALIGN, "argument plane is not element-aligned");
+        la.p[i] = static_cast<char*>(args[i]) + begin * w;
+    }
+    const uint64_t per = uint64_t(kThreads) * kPerThread;
+    const uint64_t grid = (n + per - 1) / per;
+    if (grid > 0x7fffffffull) return fail(FVB_EARG, "range too large for one launch");
+    void* params[] = {&la, &n};
+    const cudaError_t e =
+        cudaLaunchKernel(reinterpret_cast<const void*>(g->kernel), dim3(unsigned(grid)),
+                         dim3(kThreads), params, 0, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? FVB_OK : cuda_fail(e, "lowered kernel launch");
+}
+
+}  // namespace
+
+fvb_status lower_lookup(const char* key, fvb_kernel* out) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    auto it = cache().find(key);
+    if (it == cache().end()) {
+        std::string src;
+        KDag d;
+        if (!emit(key, &src, &d))
+            return fail(FVB_EUNSUPPORTED, std::string("not a loweable structural key: ") +
+                                              std::string(key).substr(0, 160));
+        std::vector<char> image;
+        if (fvb_status st = compile(src, &image)) return st;
+        auto g = std::make_unique<Gen>();
+        g->key = key;
+        g->nout = uint32_t(d.roots.size());
+        g->nin = uint32_t(d.slot_prec.size());
+        for (char p : d.dest_prec) g->arg_prec.push_back(p);
+        for (uint32_t i = 0; i < g->nin; ++i) g->arg_prec.push_back(d.slot_prec.at(int(i)));
+        cudaError_t e = cudaLibraryLoadData(&g->lib, image.data(), nullptr, nullptr, 0, nullptr,
+                                            nullptr, 0);
+        if (e == cudaSuccess) e = cudaLibraryGetKernel(&g->kernel, g->lib, "fvb_gen");
+        if (e != cudaSuccess) return cuda_fail(e, "loading the lowered kernel");
+        it = cache().emplace(key, std::move(g)).first;
+    }
+    const Gen* g = it->second.get();
+    fvb_kernel k;
+    std::memset(&k, 0, sizeof k);
+    k.fn = gen_entry;
+    k.reduce = nullptr;
+    k.n_outputs = g->nout;
+    k.n_inputs = g->nin;
+    k.n_consts = 0;
+    k.prec = g->arg_prec.empty() || g->arg_prec[0] == 'd' ? 1 : 0;
+    k.dim = 0;
+    for (int i = 0; i < 8; ++i) k.in_slot[i] = int8_t(i < int(g->nin) ? i : -1);
+    std::snprintf(k.name, sizeof k.name, "gen:%016zx", std::hash<std::string>()(g->key));
+    k.impl = g;
+    *out = k;
+    return FVB_OK;
+}
+
+}  // namespace fvb
+
+using namespace fvb;
+
+extern "C" {
+
+fvb_status fvb_emit_source(const char* key, char* buf, size_t cap, size_t* len) {
+    if (!key) return fail(FVB_EARG, "NULL key");
+    std::string src;
+    if (!emit(key, &src, nullptr))
+        return fail(FVB_EUNSUPPORTED, "not a loweable structural key");
+    if (len) *len = src.size();
+    if (buf && cap) {
+        const size_t n = src.size() < cap - 1 ? src.size() : cap - 1;
+        std::memcpy(buf, src.data(), n);
+        buf[n] = '\0';
+    }
+    return FVB_OK;
+}
+
+fvb_status fvb_nvrtc_compile(const char* key, size_t* cubin_bytes) {
+    if (!key) return fail(FVB_EARG, "NULL key");
+    std::string src;
+    if (!emit(key, &src, nullptr))
+        return fail(FVB_EUNSUPPORTED, "not a loweable structural key");
+    std::vector<char> image;
+    if (fvb_status st = compile(src, &image)) return st;
+    if (cubin_bytes) *cubin_bytes = image.size();
+    return FVB_OK;
+}
+
+}  // extern "C"

@@ -29,6 +29,7 @@
 
 #include "fvb.h"
 #include "fvb_launch.cuh"
+#include "fvb_lower.h"
 
 namespace fvb {
 namespace {
@@ -526,8 +527,8 @@ fvb_status fvb_lookup(const char* key, fvb_kernel* out) {
         *out = k;
         return FVB_OK;
     }
-    return fail(FVB_EUNSUPPORTED, std::string("no fused kernel for structural key ") +
-                                      std::string(key).substr(0, 160));
+    // No hand-written kernel: lower the tree itself (NVRTC, cached per key).
+    return lower_lookup(key, out);
 }
 
 uint32_t fvb_pattern_count(void) { return uint32_t(patterns().size()); }

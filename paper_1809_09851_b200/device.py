@@ -252,6 +252,22 @@ def lookup(key: str) -> N.KernelStruct:
     return k
 
 
+def emit_source(key: str) -> str:
+    """The CUDA source the general lowering compiles for a structural key."""
+    n = ctypes.c_size_t()
+    N.check(N.lib().fvb_emit_source(key.encode(), None, 0, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value + 1)
+    N.check(N.lib().fvb_emit_source(key.encode(), buf, n.value + 1, ctypes.byref(n)))
+    return buf.value.decode()
+
+
+def nvrtc_compile(key: str) -> int:
+    """Compile a key's lowered kernel with NVRTC (no GPU needed); cubin bytes."""
+    n = ctypes.c_size_t()
+    N.check(N.lib().fvb_nvrtc_compile(key.encode(), ctypes.byref(n)))
+    return n.value
+
+
 class HostContext:
     """fvb_ctx: the host-buffer (end-to-end) path over pinned/pageable memory."""
 

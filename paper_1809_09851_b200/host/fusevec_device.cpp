@@ -433,20 +433,32 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
     const std::size_t n = outs[0].size();
     for (const Out& o : outs)
         if (o.size() != n) throw LengthMismatch("block destinations have different lengths");
+    // Prefer a hand-written fused kernel: the whole block, else the block
+    // without its bare-leaf items (plain copies, e.g. the density that
+    // convert() passes through).  Only if neither exists, lower the whole
+    // block (fvb_lookup's NVRTC path, plan.k.impl != NULL).
     Plan plan;
-    if (!try_plan(items, outs, rows, cols, &plan)) {
-        // strip bare-leaf items (plain copies) and retry with the rest
+    const bool whole = try_plan(items, outs, rows, cols, &plan);
+    if (!whole || plan.k.impl) {
         std::vector<Expr> rest;
         std::vector<Out> rest_outs;
+        std::vector<std::pair<const DenseVector*, Out>> stripped;
         for (std::size_t i = 0; i < items.size(); ++i) {
             if (const DenseVector* src = bare_leaf(items[i].node()))
-                copies.push_back({src, outs[i]});
+                stripped.push_back({src, outs[i]});
             else {
                 rest.push_back(items[i]);
                 rest_outs.push_back(outs[i]);
             }
         }
-        if (rest.empty() || !try_plan(rest, rest_outs, rest.size(), 1, &plan)) unsupported(items);
+        Plan alt;
+        if (!stripped.empty() && !rest.empty() &&
+            try_plan(rest, rest_outs, rest.size(), 1, &alt) && (!alt.k.impl || !whole)) {
+            plan = std::move(alt);
+            copies = std::move(stripped);
+        } else if (!whole) {
+            unsupported(items);
+        }
     }
     if (need_reduce && !plan.k.reduce)
         throw UnsupportedExpression("block has no fused CFL reduction");
