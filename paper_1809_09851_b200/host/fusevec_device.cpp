@@ -268,12 +268,13 @@ struct DeviceGuard {
 // With red != nullptr the kernel's CFL reduction accumulates into it.
 void run(const DeviceBackend& be, Plan& plan, std::size_t n, void* red) {
     if (n == 0) return;
-    const std::size_t w = plan.k.prec ? sizeof(double) : sizeof(float);
-    const Precision P = plan.k.prec ? Precision::f64 : Precision::f32;
-    for (const DenseVector* l : plan.leaves)
-        if (l->precision() != P) throw UnsupportedExpression("mixed-precision leaves");
-    for (const Out& o : plan.outs)
-        if (o.prec() != P) throw UnsupportedExpression("destination precision differs");
+    // Per-slot element widths: a lowered kernel may mix f32 and f64 planes
+    // (the key carries each leaf's and each destination's precision); a
+    // hand-written kernel only ever matches uniform-precision keys.
+    std::vector<std::size_t> wl, wo;
+    for (const DenseVector* l : plan.leaves) wl.push_back(scalar_width(l->precision()));
+    for (const Out& o : plan.outs) wo.push_back(scalar_width(o.prec()));
+    constexpr std::size_t kSlotWidth = sizeof(double);  // staging slot stride per element
 
     DeviceGuard guard(be.ordinal);
     // which leaves / outputs need staging
@@ -282,7 +283,7 @@ void run(const DeviceBackend& be, Plan& plan, std::size_t n, void* red) {
     for (std::size_t i = 0; i < plan.leaves.size(); ++i) {
         DeviceVector* dv = be.residency ? be.residency->find(plan.leaves[i]) : nullptr;
         if (dv) {
-            if (dv->size() != n || dv->precision() != P)
+            if (dv->size() != n || dv->precision() != plan.leaves[i]->precision())
                 throw LengthMismatch("resident plane does not match its host leaf");
             resident_leaf[i] = dv->data();
         } else {
@@ -302,7 +303,7 @@ void run(const DeviceBackend& be, Plan& plan, std::size_t n, void* red) {
     Staging& st = staging(be.ordinal);
     std::size_t chunk = staged ? std::max<std::size_t>(be.chunk_points & ~std::size_t(63), 64) : n;
     chunk = std::min(chunk, n);
-    const std::size_t need = staged * chunk * w;
+    const std::size_t need = staged * chunk * kSlotWidth;
     if (need > st.bytes) {
         for (int b = 0; b < 2; ++b) {
             if (st.buf[b]) {
@@ -325,12 +326,12 @@ void run(const DeviceBackend& be, Plan& plan, std::size_t n, void* red) {
         std::vector<void*> leaf_ptr(plan.leaves.size());
         for (std::size_t i = 0; i < plan.leaves.size(); ++i) {
             if (resident_leaf[i]) {
-                leaf_ptr[i] = static_cast<char*>(resident_leaf[i]) + off * w;
+                leaf_ptr[i] = static_cast<char*>(resident_leaf[i]) + off * wl[i];
             } else {
-                leaf_ptr[i] = base + (slot++) * chunk * w;
+                leaf_ptr[i] = base + (slot++) * chunk * kSlotWidth;
                 cuda_check(cudaMemcpyAsync(leaf_ptr[i],
-                                           static_cast<const char*>(plan.leaves[i]->raw()) + off * w,
-                                           cnt * w, cudaMemcpyHostToDevice, s),
+                                           static_cast<const char*>(plan.leaves[i]->raw()) + off * wl[i],
+                                           cnt * wl[i], cudaMemcpyHostToDevice, s),
                            "host->device copy");
             }
         }
@@ -338,11 +339,11 @@ void run(const DeviceBackend& be, Plan& plan, std::size_t n, void* red) {
             if (plan.outs[j].is_null())
                 args[j] = nullptr;
             else if (plan.outs[j].dev)
-                args[j] = static_cast<char*>(plan.outs[j].dev->data()) + off * w;
+                args[j] = static_cast<char*>(plan.outs[j].dev->data()) + off * wo[j];
             else if (alias[j] >= 0)
                 args[j] = leaf_ptr[std::size_t(alias[j])];
             else
-                args[j] = base + (slot++) * chunk * w;
+                args[j] = base + (slot++) * chunk * kSlotWidth;
         }
         for (std::size_t i = 0; i < plan.leaves.size(); ++i) args[plan.outs.size() + i] = leaf_ptr[i];
         if (red)
@@ -351,8 +352,8 @@ void run(const DeviceBackend& be, Plan& plan, std::size_t n, void* red) {
             fvb_check(plan.k.fn(&plan.k, 0, cnt, args.data(), s));
         for (std::size_t j = 0; j < plan.outs.size(); ++j)
             if (plan.outs[j].host)
-                cuda_check(cudaMemcpyAsync(static_cast<char*>(plan.outs[j].host->raw()) + off * w,
-                                           args[j], cnt * w, cudaMemcpyDeviceToHost, s),
+                cuda_check(cudaMemcpyAsync(static_cast<char*>(plan.outs[j].host->raw()) + off * wo[j],
+                                           args[j], cnt * wo[j], cudaMemcpyDeviceToHost, s),
                            "device->host copy");
     }
     if (external) {
