@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--prec", default="f64", choices=["f64", "f32"])
     ap.add_argument("--n", type=int, default=0, help="points per GPU (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-points", type=int, default=0,
+                    help="points per rank for e2e (0: all at N=1, 2.5e7 at N>1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=10_000_000,
@@ -194,10 +196,22 @@ def end_to_end(a, fvb, ins, n, n_in, n_out, dim, dt, esize, local, dist, world, 
     fvb_jacobian_host): inputs copied from pinned host memory and every
     computed output plane copied back, all inside the timed region.  The
     flux's row 0 (bit-for-bit the momentum inputs) is copied host-side by the
-    library instead of crossing PCIe; it is counted separately."""
+    library instead of crossing PCIe; it is counted separately.
+
+    Host memory: one rank pins (n_in + n_out) planes.  With several ranks per
+    box each streams a bounded slice (--e2e-points, default 2.5e7 points per
+    rank when N > 1) -- the pipeline's rate is flat in the point count far
+    below that -- so 8 ranks never pin more than ~32 GB between them."""
+    if world > 1 and a.e2e_points == 0:
+        n = min(n, 25_000_000)
+    elif a.e2e_points:
+        n = min(n, a.e2e_points)
     torch.cuda.empty_cache()
-    host_in = [t.cpu().pin_memory() for t in ins]
-    host_out = [torch.empty(n, dtype=dt).pin_memory() for _ in range(n_out)]
+    host_in = torch.empty((n_in, n), dtype=dt).pin_memory()
+    for i, t in enumerate(ins):
+        host_in[i].copy_(t[:n])
+    host_in = list(host_in.unbind(0))
+    host_out = list(torch.empty((n_out, n), dtype=dt).pin_memory().unbind(0))
     ctx = fvb.HostContext(local)
 
     def e2e_step():
@@ -225,6 +239,7 @@ def end_to_end(a, fvb, ins, n, n_in, n_out, dim, dt, esize, local, dist, world, 
                                   + (8 if a.config == "jacobian3d" else 0),
             "host_passthrough_bytes_per_step": world * n * passthrough * esize,
             "ms_per_step": e2e_s * 1e3, "host_memory": "pinned", "steps": a.e2e_steps,
+            "points_per_rank": n,
             "path": "fvb_flux_host" if a.config == "flux3d" else "fvb_jacobian_host"}
 
 

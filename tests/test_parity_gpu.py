@@ -377,3 +377,24 @@ def test_cuda_graph_capture(cuda, orc):
     torch.cuda.synchronize()
     want = orc.flux(dim, [t.cpu().numpy() for t in s])
     assert all_same(to_host(out), want)
+
+
+# ---- IEEE special values -----------------------------------------------------------
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("dim", [1, 2, 3])
+def test_special_values(cuda, orc, prec, dim):
+    # zero / negative density, +-0, +-inf, NaN, the smallest denormal:
+    # bitwise except NaN payloads (both NaN suffices), like the oracle vs the
+    # reference (test_oracle.py::test_special_values_vs_reference)
+    from tests.test_oracle import nan_aware_equal, special_state
+    s_np = special_state(dim, prec)
+    s = to_dev(s_np, cuda)
+    for got, want in [(fvb.flux(s, dim), orc.flux(dim, s_np)),
+                      (fvb.cons2prim(s, dim), orc.cons2prim(dim, s_np)),
+                      (fvb.jacobian(s, dim)[0], orc.jacobian(dim, s_np)[0])]:
+        got = to_host(got)
+        assert all(nan_aware_equal(x, y) for x, y in zip(got, want))
+    _, lam = fvb.wave_speed_max(s, dim)
+    assert np.isnan(lam.item())
