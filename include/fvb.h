@@ -152,6 +152,18 @@ FVB_API fvb_status fvb_wave_speed_max(const fvb_gas* gas, uint32_t dim, uint8_t 
                               const void* const* in, void* lambda, void* lambda_max,
                               void* stream);
 
+/* CSR sparse matrix-vector accumulation of the block layer (paper Eq. 2;
+ * csr_matvec_acc, src/block.cpp:345-357): y[r] += sum_k (TY)v[k]*(TY)x[ci[k]]
+ * for r < rows, the row's nonzeros summed in stored order in y's precision
+ * (bitwise the reference's order).  row_ptr (rows+1 entries), col_idx and
+ * values (nnz entries, already narrowed to the matrix precision as
+ * SparseMatrix stores them) are DEVICE arrays; x and y device planes of
+ * precisions prec_x / prec_y. */
+FVB_API fvb_status fvb_csr_matvec_acc(uint8_t prec_y, uint8_t prec_x, uint64_t rows, uint64_t nnz,
+                                      const uint64_t* row_ptr, const uint64_t* col_idx,
+                                      const double* values, const void* x, void* y,
+                                      void* stream);
+
 /* On-device synthetic inputs, bit-identical to the reference's host
  * generators because SplitMix64 is random-access (proj/include/fusevec/
  * rng.hpp:8-28):

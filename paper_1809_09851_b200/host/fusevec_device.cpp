@@ -400,6 +400,90 @@ bool try_plan(const std::vector<Expr>& items, std::vector<Out> outs, std::size_t
                                 " (general lowering is not implemented; no CPU fallback)");
 }
 
+// A device allocation freed on scope exit.
+struct DevBuf {
+    void* p = nullptr;
+    explicit DevBuf(std::size_t bytes) {
+        if (bytes) cuda_check(cudaMalloc(&p, bytes), "device allocation");
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+// CSR block-matvec rows (proj/src/block.cpp:389-411, 429-447): each row item
+// y = sum_t M_t * eval(op_t) in the destination's precision.  Operands are
+// device planes: a bare leaf is used in place when resident (else uploaded
+// once), any other operand expression is evaluated once on the device into
+// a scratch plane -- the reference's "one scratch per distinct operand".
+void run_matvec(const DeviceBackend& be, std::vector<std::pair<const BlockItem*, Out>>& mv) {
+    DeviceGuard guard(be.ordinal);
+    cudaStream_t s = static_cast<cudaStream_t>(be.stream);
+    std::map<const ExprNode*, std::unique_ptr<DeviceVector>> owned;
+    std::map<const ExprNode*, const DeviceVector*> planes;
+    auto operand = [&](const Expr& op, std::size_t cols) -> const DeviceVector& {
+        const ExprNode* key = op.ptr().get();
+        auto it = planes.find(key);
+        if (it != planes.end()) return *it->second;
+        if (const DenseVector* lf = bare_leaf(op.node())) {
+            if (lf->size() != cols)
+                throw LengthMismatch("matvec column count " + std::to_string(cols) +
+                                     " vs operand length " + std::to_string(lf->size()));
+            if (DeviceVector* dv = be.residency ? be.residency->find(lf) : nullptr)
+                return *(planes[key] = dv);
+            auto t = std::make_unique<DeviceVector>(lf->precision(), lf->size());
+            t->upload(*lf);
+            planes[key] = t.get();
+            return *(owned[key] = std::move(t));
+        }
+        auto t = std::make_unique<DeviceVector>(op.result_precision(), cols);
+        evaluate(be, op, *t);
+        planes[key] = t.get();
+        return *(owned[key] = std::move(t));
+    };
+    for (auto& [item, d] : mv) {
+        const std::size_t rows = d.size();
+        std::unique_ptr<DeviceVector> tmp;
+        DeviceVector* y = d.dev;
+        if (!y) {
+            tmp = std::make_unique<DeviceVector>(d.prec(), rows);
+            y = tmp.get();
+        }
+        if (rows) cuda_check(cudaMemsetAsync(y->data(), 0, y->byte_size(), s), "matvec reset");
+        for (const MatVecTerm& t : item->terms()) {
+            if (t.mat->rows() != rows)
+                throw LengthMismatch("matvec row count " + std::to_string(t.mat->rows()) +
+                                     " vs destination length " + std::to_string(rows));
+            const DeviceVector& x = operand(t.operand, t.mat->cols());
+            if (x.size() != t.mat->cols())
+                throw LengthMismatch("matvec column count " + std::to_string(t.mat->cols()) +
+                                     " vs operand length " + std::to_string(x.size()));
+            const auto& rp = t.mat->row_ptr();
+            const auto& ci = t.mat->col_idx();
+            const auto& v = t.mat->values();
+            static_assert(sizeof(std::size_t) == sizeof(uint64_t), "64-bit size_t");
+            DevBuf drp(rp.size() * 8), dci(ci.size() * 8), dv(v.size() * 8);
+            if (!rp.empty())
+                cuda_check(cudaMemcpyAsync(drp.p, rp.data(), rp.size() * 8, cudaMemcpyHostToDevice, s), "csr upload");
+            if (!ci.empty()) {
+                cuda_check(cudaMemcpyAsync(dci.p, ci.data(), ci.size() * 8, cudaMemcpyHostToDevice, s), "csr upload");
+                cuda_check(cudaMemcpyAsync(dv.p, v.data(), v.size() * 8, cudaMemcpyHostToDevice, s), "csr upload");
+            }
+            fvb_check(fvb_csr_matvec_acc(y->precision() == Precision::f64 ? 1 : 0,
+                                         x.precision() == Precision::f64 ? 1 : 0, rows, ci.size(),
+                                         static_cast<const uint64_t*>(drp.p),
+                                         static_cast<const uint64_t*>(dci.p),
+                                         static_cast<const double*>(dv.p), x.data(), y->data(), s));
+            cuda_check(cudaStreamSynchronize(s), "matvec");  // before the CSR buffers go
+        }
+        if (d.host && rows)
+            cuda_check(cudaMemcpy(d.host->raw(), y->data(), y->byte_size(), cudaMemcpyDeviceToHost),
+                       "matvec read-back");
+    }
+}
+
 // Shared body of the evaluate_block overloads.
 void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, std::size_t cols,
                 const std::vector<Out>& dests_in, void* red, bool need_reduce) {
@@ -410,6 +494,7 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
     std::vector<Expr> items;
     std::vector<Out> outs;
     std::vector<std::pair<const DenseVector*, Out>> copies;  // bare-leaf items
+    std::vector<std::pair<const BlockItem*, Out>> matvecs;   // CSR block-matvec rows
     std::size_t idx = 0;
     for (std::size_t r = 0; r < rows; ++r)
         for (std::size_t c = 0; c < cols; ++c, ++idx) {
@@ -418,9 +503,12 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
             switch (it.kind()) {
                 case ItemKind::Expression: x = it.expr(); break;
                 case ItemKind::Vector: x = leaf(it.vector()); break;
-                default:
-                    throw UnsupportedExpression(
-                        "sparse-matrix block items are not on the device path");
+                case ItemKind::MatVec:
+                    if (need_reduce) throw UnsupportedExpression("matvec block has no CFL reduction");
+                    matvecs.push_back({&it, dests_in[idx]});
+                    continue;
+                default:  // as the reference: proj/src/block.cpp:427-428
+                    throw KindMismatch("cannot assign a sparse-matrix item into a vector");
             }
             const Out& d = dests_in[idx];
             std::map<int, const DenseVector*> tags;
@@ -430,7 +518,14 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
             items.push_back(x);
             outs.push_back(d);
         }
+    // Matvec rows first: their operands are captured before any destination
+    // of this block is written (the reference's scratch pass, block.cpp:389-411).
+    if (!matvecs.empty()) run_matvec(be, matvecs);
     if (items.empty()) return;
+    if (!matvecs.empty()) {  // the fused key covers only the element-wise items
+        rows = items.size();
+        cols = 1;
+    }
     const std::size_t n = outs[0].size();
     for (const Out& o : outs)
         if (o.size() != n) throw LengthMismatch("block destinations have different lengths");

@@ -353,6 +353,73 @@ void run_gpu() {
         return "max ulp: " + report;
     });
 
+    check("criterion 7 on device: CSR block matvec, all shapes <= 3x3, dims <= 8, bitwise", [&] {
+        // acceptance.cpp:343-379 builds random sparse blocks and compares to a
+        // dense oracle within 1e-12; the device path must equal the
+        // reference's own evaluate_block bit for bit (same summation order).
+        SplitMix64 rng(0xB10C);
+        int cases = 0;
+        for (std::size_t br = 1; br <= 3; ++br)
+            for (std::size_t bc = 1; bc <= 3; ++bc)
+                for (std::size_t n = 1; n <= 8; n += 3)
+                    for (std::size_t m = 1; m <= 8; m += 3) {
+                        std::vector<SparseMatrix> blocks;
+                        for (std::size_t i = 0; i < br * bc; ++i) {
+                            std::vector<Triplet> trips;
+                            for (std::size_t r = 0; r < n; ++r)
+                                for (std::size_t c = 0; c < m; ++c)
+                                    if (rng.uniform() < 0.5)
+                                        trips.push_back({r, c, rng.uniform(-2.0, 2.0)});
+                            blocks.emplace_back(n, m, trips);
+                        }
+                        BlockMatrix mat(br, bc, std::move(blocks));
+                        std::vector<DenseVector> x;
+                        std::vector<BlockItem> xi;
+                        for (std::size_t c = 0; c < bc; ++c)
+                            x.push_back(testutil::make_vec(Precision::f64, m, rng, -2.0, 2.0));
+                        for (auto& v : x) xi.push_back(BlockItem(v));
+                        BlockExpr prod = block_matvec(mat, BlockExpr(bc, 1, std::move(xi)));
+                        std::vector<DenseVector> wd, gd;
+                        for (std::size_t r = 0; r < br; ++r) {
+                            wd.emplace_back(Precision::f64, n);
+                            gd.emplace_back(Precision::f64, n);
+                        }
+                        BlockColVector want(std::move(wd)), got(std::move(gd));
+                        evaluate_block(ref, prod, want);
+                        dev::evaluate_block(be, prod, got);
+                        for (std::size_t r = 0; r < br; ++r)
+                            if (!same_bits(want.get(r), got.get(r))) fail("matvec differs");
+                        ++cases;
+                    }
+        // identity blocks with expression operands (acceptance.cpp:381-395):
+        // y = [I I; I I] [sin(x0+x1); cos(x0-x1)] at x = 0 is all ones
+        const std::size_t n = 8;
+        std::vector<Triplet> diag;
+        for (std::size_t i = 0; i < n; ++i) diag.push_back({i, i, 1.0});
+        SparseMatrix ident(n, n, diag);
+        BlockMatrixView mv(2, 2, {&ident, &ident, &ident, &ident});
+        DenseVector x0(Precision::f64, n), x1(Precision::f64, n);
+        BlockExpr rhs = make_block_expr(2, 1, elem_sin(leaf(x0) + leaf(x1)),
+                                        elem_cos(leaf(x0) - leaf(x1)));
+        BlockColVector y({DenseVector(Precision::f64, n), DenseVector(Precision::f64, n)});
+        dev::evaluate_block(be, block_matvec(mv, rhs), y);
+        for (std::size_t r = 0; r < 2; ++r)
+            for (std::size_t i = 0; i < n; ++i)
+                if (y.get(r).at(i) != 1.0) fail("identity-blocks case is not all ones");
+        // f32 destination, f64 operand: accumulation in the destination's precision
+        SparseMatrix a(4, 3, {{0, 0, 0.1}, {0, 2, 0.3}, {2, 1, -0.7}, {3, 2, 1.5}}, Precision::f32);
+        DenseVector xv = testutil::make_vec(Precision::f64, 3, rng);
+        std::vector<DenseVector> w32, g32;
+        w32.emplace_back(Precision::f32, 4);
+        g32.emplace_back(Precision::f32, 4);
+        BlockColVector w3(std::move(w32)), g3(std::move(g32));
+        BlockExpr p32 = block_matvec(BlockMatrixView(1, 1, a), make_block_expr(1, 1, leaf(xv)));
+        evaluate_block(ref, p32, w3);
+        dev::evaluate_block(be, p32, g3);
+        if (!same_bits(w3.get(0), g3.get(0))) fail("mixed-precision matvec differs");
+        return std::to_string(cases) + " random block shapes bitwise; identity case all ones";
+    });
+
     check("criterion 6 on device: flux, d in {1,2,3} x 100 instances, n=64, bitwise", [&] {
         SplitMix64 rng(0xF1);
         for (std::size_t d = 1; d <= 3; ++d)
@@ -533,17 +600,16 @@ void run_gpu() {
         }
         if (!threw) fail("non-finite constant did not throw UnsupportedExpression");
         threw = false;
-        try {  // sparse-matrix block items stay on the host path
+        try {  // a bare sparse-matrix item has no vector value (block.cpp:427-428)
             SparseMatrix m(10, 10, {{0, 0, 1.0}});
             std::vector<DenseVector> col;
             col.emplace_back(Precision::f64, 10);
             BlockColVector y(std::move(col));
-            dev::evaluate_block(be, block_matvec(BlockMatrixView(1, 1, m),
-                                                 make_block_expr(1, 1, leaf(a))), y);
-        } catch (const UnsupportedExpression&) {
+            dev::evaluate_block(be, make_block_expr(1, 1, m), y);
+        } catch (const KindMismatch&) {
             threw = true;
         }
-        if (!threw) fail("matvec did not throw UnsupportedExpression");
+        if (!threw) fail("matrix item did not throw KindMismatch");
         threw = false;
         try {
             dev::evaluate(be, constant(0.5, leaf(a)) * elem_sin(leaf(a) + leaf(b)), out);

@@ -30,4 +30,4 @@ def test_reference_trees_resolve_to_fused_kernels():
 @pytest.mark.gpu
 def test_reference_api_on_device(cuda):
     out = run("gpu")
-    assert out.count("[PASS]") == 10
+    assert out.count("[PASS]") == 12
