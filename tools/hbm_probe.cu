@@ -91,6 +91,49 @@ __global__ void __launch_bounds__(256) stream_kernel(P<R, W> p, unsigned long lo
     } else if (MODE == 1) {
         const unsigned long long g = (unsigned long long)blockIdx.x * blockDim.x * U + threadIdx.x;
         body<R, W, V, U>(p, g, blockDim.x, groups, acc);
+    } else if constexpr (MODE == 3 && V == 4) {
+        // one-shot tiles, stores through shared memory + TMA bulk copies:
+        // each warp stages its 1 KB of output plane j and one lane issues a
+        // cp.async.bulk shared->global copy (4-slot ring per warp).
+        __shared__ __align__(128) double stage[8][4][128];
+        const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const unsigned long long g = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+        const unsigned long long wg0 = (unsigned long long)blockIdx.x * blockDim.x + warp * 32;
+        if (wg0 + 32 > groups) {
+            body<R, W, V, 1>(p, g, blockDim.x, groups, acc);
+        } else {
+            double x[R][V];
+#pragma unroll
+            for (int i = 0; i < R; ++i) ldv<V>(p.in[i] + g * V, x[i]);
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                const int slot = j & 3;
+                if (j >= 4) {
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+                    __syncwarp();
+                }
+                double* s = &stage[warp][slot][lane * 4];
+                const double* src = x[j % R];
+                s[0] = src[0];
+                s[1] = src[1];
+                s[2] = src[2];
+                s[3] = src[3];
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    const unsigned saddr =
+                        static_cast<unsigned>(__cvta_generic_to_shared(&stage[warp][slot][0]));
+                    asm volatile(
+                        "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 1024;" ::"l"(
+                            p.out[j] + wg0 * 4),
+                        "r"(saddr)
+                        : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            }
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            __syncwarp();
+        }
     } else {
         const unsigned long long per = (groups + gridDim.x - 1) / gridDim.x;
         const unsigned long long lo = blockIdx.x * per;
@@ -117,8 +160,9 @@ void run(const std::vector<double*>& bufs, size_t n, int sms) {
     auto k = stream_kernel<R, W, V, U, MODE>;
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
-    unsigned grid = MODE == 1 ? unsigned((groups + 256ull * U - 1) / (256ull * U))
-                              : unsigned(sms * per_sm);
+    unsigned grid = (MODE == 1 || MODE == 3)
+                        ? unsigned((groups + 256ull * U - 1) / (256ull * U))
+                        : unsigned(sms * per_sm);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
@@ -150,6 +194,7 @@ void sweep(const std::vector<double*>& bufs, size_t n, int sms) {
     run<R, W, 2, 4, 1>(bufs, n, sms);
     run<R, W, 4, 1, 2>(bufs, n, sms);
     run<R, W, 4, 2, 2>(bufs, n, sms);
+    if constexpr (W > 0) run<R, W, 4, 1, 3>(bufs, n, sms);
 }
 
 int main(int argc, char** argv) {
@@ -168,5 +213,17 @@ int main(int argc, char** argv) {
     sweep<3, 3>(bufs, n, sms);   // 1D cons->prim
     sweep<2, 1>(bufs, n, sms);   // axpy-sin
     sweep<5, 0>(bufs, n, sms);   // read-only CFL pass
+    // 3-D Jacobians: 80 planes, at a quarter of N
+    for (double* b : bufs) cudaFree(b);
+    const size_t nj = (n / 4) & ~size_t(15);
+    std::vector<double*> jb(81);
+    for (int i = 0; i < 81; ++i) {
+        if (cudaMalloc(&jb[i], nj * 8) != cudaSuccess) return 1;
+        fill<<<sms * 8, 256>>>(jb[i], nj, i);
+    }
+    cudaDeviceSynchronize();
+    run<5, 75, 4, 1, 1>(jb, nj, sms);
+    run<5, 75, 4, 1, 3>(jb, nj, sms);
+    run<5, 75, 4, 1, 0>(jb, nj, sms);
     return 0;
 }
