@@ -31,3 +31,16 @@ def test_reference_trees_resolve_to_fused_kernels():
 def test_reference_api_on_device(cuda):
     out = run("gpu")
     assert out.count("[PASS]") == 12
+
+
+def test_adapter_compiles_in_the_references_own_namespace():
+    # A maintainer compiles the adapter into fusevec itself,
+    # i.e. without the test build's -Dfusevec=fvref rename.
+    inc = "/root/reference/proj/include"
+    if not os.path.isdir(inc):
+        pytest.skip("reference headers not mounted")
+    src = os.path.join(ROOT, "paper_1809_09851_b200", "host", "fusevec_device.cpp")
+    p = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Werror", f"-I{inc}",
+                        f"-I{ROOT}/include", f"-I{ROOT}/paper_1809_09851_b200/host",
+                        "-I/usr/local/cuda/include", src], capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr
