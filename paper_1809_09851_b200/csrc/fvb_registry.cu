@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -498,6 +499,13 @@ extern "C" {
 
 fvb_status fvb_lookup(const char* key, fvb_kernel* out) {
     if (!key || !out) return fail(FVB_EARG, "NULL key or output");
+    // FVB_FORCE_LOWER=1 skips the hand-written kernels (tests and the
+    // hand-written-vs-lowered comparison run the same trees both ways).
+    static const bool force_lower = [] {
+        const char* v = std::getenv("FVB_FORCE_LOWER");
+        return v && *v && *v != '0';
+    }();
+    if (force_lower) return lower_lookup(key, out);
     for (const Pattern& p : patterns()) {
         double consts[8] = {0};
         bool seen[8] = {false};

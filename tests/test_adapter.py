@@ -33,6 +33,16 @@ def test_reference_api_on_device(cuda):
     assert out.count("[PASS]") == 12
 
 
+@pytest.mark.gpu
+def test_reference_api_on_device_all_lowered(cuda, monkeypatch):
+    # The same acceptance checks with every tree -- flux, conversions,
+    # Jacobians -- run through the general NVRTC lowering instead of the
+    # hand-written kernels: still bitwise against the reference engine.
+    monkeypatch.setenv("FVB_FORCE_LOWER", "1")
+    out = run("gpu")
+    assert out.count("[PASS]") == 12
+
+
 def test_adapter_compiles_in_the_references_own_namespace():
     # A maintainer compiles the adapter into fusevec itself,
     # i.e. without the test build's -Dfusevec=fvref rename.
