@@ -205,7 +205,8 @@ struct fvb_kernel {
     uint32_t n_consts;   /* valid entries of consts                           */
     uint8_t prec;        /* precision of every slot (0 f32, 1 f64)            */
     uint8_t dim;         /* spatial dimension of a fluid block (0 otherwise)  */
-    int8_t in_slot[8];   /* canonical input i is args[n_outputs + in_slot[i]] */
+    int8_t in_slot[8];   /* canonical input i is args[n_outputs + in_slot[i]];
+                            all -1 for a lowered kernel (no canonical order)  */
     double consts[8];    /* captured constants, named per kernel  */
     char name[48];       /* e.g. "flux3_f64", or "gen:<hash>" when lowered    */
     const void* impl;    /* opaque: the NVRTC-lowered kernel, else NULL       */

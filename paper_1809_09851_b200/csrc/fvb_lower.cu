@@ -459,7 +459,9 @@ fvb_status lower_lookup(const char* key, fvb_kernel* out) {
     k.n_consts = 0;
     k.prec = g->arg_prec.empty() || g->arg_prec[0] == 'd' ? 1 : 0;
     k.dim = 0;
-    for (int i = 0; i < 8; ++i) k.in_slot[i] = int8_t(i < int(g->nin) ? i : -1);
+    // A lowered kernel has no canonical input order: it takes its leaves in
+    // the key's slot order, which is exactly the jit_args order.
+    for (int i = 0; i < 8; ++i) k.in_slot[i] = -1;
     std::snprintf(k.name, sizeof k.name, "gen:%016zx", std::hash<std::string>()(g->key));
     k.impl = g;
     *out = k;

@@ -32,7 +32,7 @@ def key_of(pattern):
     return re.sub(r"C([sd])#(\w+);", sub, pattern)
 
 
-def run_one(name, n, dump):
+def run_one(name, n, dump, slot_map):
     import ctypes
 
     import numpy as np
@@ -45,9 +45,12 @@ def run_one(name, n, dump):
     k = fvb.lookup(key_of(dict(fvb.patterns())[name]))
     state = fvb.synth_state(dim, n, seed=0x5EED)
     outs = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(nout)]
+    # canonical plane c -> argument slot, from the hand-written kernel's
+    # in_slot (the key's first-appearance leaf order; a lowered kernel takes
+    # its arguments in that same slot order)
     slots = [None] * k.n_inputs
     for c in range(nin):
-        slots[k.in_slot[c]] = state[c]
+        slots[slot_map[c]] = state[c]
     args = N.ptr_array([t.data_ptr() for t in outs + slots])
     s = torch.cuda.current_stream().cuda_stream
     for _ in range(3):
@@ -72,19 +75,24 @@ def main():
     ap.add_argument("--n", type=int, default=100_000_000)
     ap.add_argument("--child", default="")
     ap.add_argument("--dump", default="")
+    ap.add_argument("--slots", default="")
     a = ap.parse_args()
     if a.child:
-        print(json.dumps(run_one(a.child, a.n, a.dump)))
+        print(json.dumps(run_one(a.child, a.n, a.dump, [int(x) for x in a.slots.split(",")])))
         return
     import numpy as np
+
+    import paper_1809_09851_b200 as fvb
 
     for name in BLOCKS:
         n = a.n if name != "jacobian3_f64" else a.n // 4
         res = {}
+        hw = fvb.lookup(key_of(dict(fvb.patterns())[name]))
+        slot_map = ",".join(str(hw.in_slot[c]) for c in range(BLOCKS[name][1]))
         for mode, env in (("handwritten", {}), ("lowered", {"FVB_FORCE_LOWER": "1"})):
             dump = f"/tmp/lvh_{name}_{mode}.npy"
             p = subprocess.run([sys.executable, __file__, "--child", name, "--n", str(n),
-                                "--dump", dump], capture_output=True, text=True,
+                                "--dump", dump, "--slots", slot_map], capture_output=True, text=True,
                                env={**os.environ, **env})
             if p.returncode != 0:
                 res[mode] = {"error": p.stderr[-400:]}
