@@ -43,6 +43,8 @@ CONFIGS = {
     "cons2prim1d": (1, 3, 3, 100_000_000, "C2: 1D cons->prim + ideal-gas p + sound speed"),
     "jacobian3d": (3, 5, 75, 100_000_000, "C4: 3D 5x5 flux Jacobians x3 + CFL max allreduce"),
     "axpy": (0, 2, 1, 1_000_000, "C1: UETLI y = 0.5*sin(x+y)"),
+    "vmag2": (3, 4, 1, 100_000_000,
+              "paper micro-benchmark (mx^2+my^2+mz^2)/rho^2 = derived_v_mag2, 3D"),
 }
 
 
@@ -52,7 +54,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fvb", choices=["fvb", "reference"])
-    ap.add_argument("--config", default="flux3d", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="flux3d", choices=sorted(CONFIGS))  # noqa: E501
     ap.add_argument("--prec", default="f64", choices=["f64", "f32"])
     ap.add_argument("--n", type=int, default=0, help="points per GPU (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -163,7 +165,7 @@ class ClockSampler:
 
 # ---- the reference arm (CPU) -----------------------------------------------------------
 
-REF_WHICH = {"flux3d": 0, "cons2prim1d": 1, "jacobian3d": 2, "axpy": 3}
+REF_WHICH = {"flux3d": 0, "cons2prim1d": 1, "jacobian3d": 2, "axpy": 3, "vmag2": 4}
 
 
 def reference_run(cfg_name, prec, steps, warmup, sample, threads):
@@ -287,6 +289,8 @@ def device_run(a, rank, world, local):
             fvb.cons2prim(ins, dim, out=outs, stream=stream)
         elif a.config == "jacobian3d":
             fvb.jacobian(ins, dim, out=outs, lambda_max=lam, stream=stream)
+        elif a.config == "vmag2":
+            fvb.v_mag2(ins, dim, out=outs[0], stream=stream)
         else:
             fvb.axpy_sin(ins[0], ins[1], stream=stream)
 

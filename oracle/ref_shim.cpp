@@ -382,6 +382,12 @@ int fvr_time_config(int which, int dim, int prec, std::uint64_t n, int workers, 
             run();
             for (int r = 0; r < reps; ++r) times_ns[r] = time_ns(run);
             (void)sink;
+        } else if (which == 4) {
+            // the paper's micro-benchmark: derived_v_mag2 (bench.cpp:153-206)
+            Expr vm = derived_v_mag2(u);
+            DenseVector out(P, n);
+            evaluate(be, vm, out);
+            for (int r = 0; r < reps; ++r) times_ns[r] = time_ns([&] { evaluate(be, vm, out); });
         } else {
             throw Error("unknown timing config");
         }

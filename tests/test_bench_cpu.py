@@ -43,7 +43,7 @@ def test_warmup_floor():
     assert p.returncode != 0
 
 
-@pytest.mark.parametrize("config", ["cons2prim1d", "jacobian3d", "axpy"])
+@pytest.mark.parametrize("config", ["cons2prim1d", "jacobian3d", "axpy", "vmag2"])
 def test_reference_arm_other_configs(ref, config):
     p = run(["--impl", "reference", "--config", config, "--steps", "3", "--warmup", "3",
              "--cpu-sample", "5000", "--n", "5000"])

@@ -398,3 +398,27 @@ def test_special_values(cuda, orc, prec, dim):
         assert all(nan_aware_equal(x, y) for x, y in zip(got, want))
     _, lam = fvb.wave_speed_max(s, dim)
     assert np.isnan(lam.item())
+
+
+def test_cons2prim_1e8_sampled_and_round_trip(cuda, orc):
+    # C2 at N = 1e8: sampled points bitwise against the oracle at the same
+    # global points; over all 1e8 points the size-independent property
+    # prim2cons(cons2prim(U)) == U within 1e-12 (acceptance.cpp:244-284).
+    dim, n = 1, 100_000_000
+    s = fvb.synth_state(dim, n, seed=0x5EED)
+    c = fvb.cons2prim(s, dim)
+    back = fvb.prim2cons([s[0], c[0], c[1]], dim)
+    torch.cuda.synchronize()
+    for a, b in zip(back, s[1:]):
+        scale = torch.clamp(torch.maximum(a.abs(), b.abs()), min=1.0)
+        assert bool(((a - b).abs() <= 1e-12 * scale).all())
+    rng = np.random.default_rng(2)
+    idx = np.unique(np.concatenate([rng.integers(0, n, 2000), [0, n - 1]]))
+    it = torch.from_numpy(idx).to(cuda)
+    got = np.stack([t[it].cpu().numpy() for t in c])
+    for k, i in enumerate(idx):
+        pt = orc.random_state(dim, 1, seed=0x5EED, first=int(i))
+        want = np.array([a[0] for a in orc.cons2prim(dim, pt)])
+        assert same_bits(got[:, k], want), int(i)
+    del s, c, back
+    torch.cuda.empty_cache()
