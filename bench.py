@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fvb", choices=["fvb", "reference"])
-    ap.add_argument("--config", default="flux3d", choices=sorted(CONFIGS))  # noqa: E501
+    ap.add_argument("--config", default="flux3d", choices=sorted(CONFIGS))
     ap.add_argument("--prec", default="f64", choices=["f64", "f32"])
     ap.add_argument("--n", type=int, default=0, help="points per GPU (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=3)

@@ -20,8 +20,6 @@ namespace {
 thread_local std::string t_error;
 }
 
-void set_error(const std::string& msg) { t_error = msg; }
-
 fvb_status fail(fvb_status s, const std::string& msg) {
     t_error = msg;
     return s;

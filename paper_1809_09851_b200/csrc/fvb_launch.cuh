@@ -17,7 +17,6 @@
 namespace fvb {
 
 // Per-thread error message behind fvb_last_error().
-void set_error(const std::string& msg);
 fvb_status fail(fvb_status s, const std::string& msg);
 fvb_status cuda_fail(cudaError_t e, const char* what);
 

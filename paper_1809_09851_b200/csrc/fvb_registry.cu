@@ -63,17 +63,11 @@ N neg(N a) { return un(kNeg, a); }
 struct Render {
     char p;                          // precision char, 'd' or 's'
     std::vector<std::string> slots;  // leaf names in first-appearance order
-    std::vector<std::string> consts; // constant names in first-appearance order
     int slot_of(const std::string& n) {
         for (size_t i = 0; i < slots.size(); ++i)
             if (slots[i] == n) return int(i);
         slots.push_back(n);
         return int(slots.size() - 1);
-    }
-    void note_const(const std::string& n) {
-        for (const auto& c : consts)
-            if (c == n) return;
-        consts.push_back(n);
     }
     // key_node (proj/src/backend_jit.cpp:112-155) over a uniform-precision tree.
     void node(const Node& n, std::string& out) {
@@ -85,7 +79,6 @@ struct Render {
                 out += ';';
                 return;
             case 'C':
-                note_const(n.name);
                 out += 'C';
                 out += p;
                 out += '#';
@@ -366,7 +359,7 @@ void add_fluid(std::vector<Pattern>& ps) {
     const Cons u(D);
     auto block = [&](const std::string& name, int rows, int cols, const std::vector<N>& items,
                      std::vector<std::string> canon, fvb_kernel_fn fn) {
-        Render r{pc, {}, {}};
+        Render r{pc, {}};
         Pattern p{name + sfx, r.block(rows, cols, items), {}, std::move(canon),
                   uint32_t(items.size()), uint8_t(sizeof(T) == 8), uint8_t(D), fn};
         p.slots = r.slots;
@@ -374,7 +367,7 @@ void add_fluid(std::vector<Pattern>& ps) {
     };
     auto single = [&](const std::string& name, const N& e, std::vector<std::string> canon,
                       fvb_kernel_fn fn) {
-        Render r{pc, {}, {}};
+        Render r{pc, {}};
         Pattern p{name + sfx, r.expr(e), {}, std::move(canon), 1u, uint8_t(sizeof(T) == 8),
                   uint8_t(D), fn};
         p.slots = r.slots;
@@ -403,7 +396,7 @@ void add_scalar(std::vector<Pattern>& ps) {
     const std::string sfx = sizeof(T) == 8 ? "_f64" : "_f32";
     auto single = [&](const std::string& name, const N& e, std::vector<std::string> canon,
                       fvb_kernel_fn fn) {
-        Render r{pc, {}, {}};
+        Render r{pc, {}};
         Pattern p{name + sfx, r.expr(e), {}, std::move(canon), 1u, uint8_t(sizeof(T) == 8), 0,
                   fn};
         p.slots = r.slots;
@@ -422,7 +415,7 @@ void add_scalar(std::vector<Pattern>& ps) {
 template <class T>
 void add_eos_T(std::vector<Pattern>& ps) {
     const char pc = sizeof(T) == 8 ? 'd' : 's';
-    Render r{pc, {}, {}};
+    Render r{pc, {}};
     Pattern p{std::string("eos_T") + (sizeof(T) == 8 ? "_f64" : "_f32"),
               r.expr(dvd(leaf("e"), cst("cv"))), {}, {"e", "e"}, 1u, uint8_t(sizeof(T) == 8), 0,
               entry<EosOp<T, 2>, T>};
