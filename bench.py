@@ -262,7 +262,10 @@ def device_run(a, rank, world, local):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     dist = None
-    if world > 1:
+    # Under torchrun (WORLD_SIZE set) the process group is initialised even
+    # for one rank, so the barrier / max-over-ranks / allreduce code is the
+    # same at N = 1 as at N = 8.
+    if world > 1 or "WORLD_SIZE" in os.environ:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     outs = None
@@ -423,6 +426,11 @@ def device_run(a, rank, world, local):
 def main():
     a = parse()
     rank, world, local = dist_env()
+    # stdout carries exactly one JSON line: everything else any library
+    # prints to fd 1 (e.g. NCCL's version banner at init) goes to stderr.
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
     if a.impl == "reference":
         if rank != 0:
             return 0
@@ -461,7 +469,8 @@ def main():
         line = device_run(a, rank, world, local)
     if rank == 0:
         text = json.dumps(line)
-        print(text, flush=True)
+        sys.stdout.flush()
+        os.write(json_fd, (text + "\n").encode())
         if a.out:
             with open(a.out, "a") as f:
                 f.write(text + "\n")
