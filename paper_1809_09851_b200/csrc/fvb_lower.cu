@@ -281,12 +281,52 @@ bool emit(const char* key, std::string* src, KDag* dag_out) {
     Emitter e(d);
     std::vector<std::string> roots;
     for (int r : d.roots) roots.push_back(e.as(d.dest_prec[roots.size()], r));
+    // a register cap of 128 (2 CTAs/SM) for trees small enough not to spill
+    const int minb = int(d.nodes.size()) + nout <= 48 ? 2 : 1;
+    const std::string T = std::to_string(kThreads);
     std::string s;
     s += "// lowered by libfvb from a structural key (proj/src/backend_jit.cpp grammar)\n";
     s += "typedef unsigned long long fvb_u64;\n";
     s += "struct FvbArgs { void* p[" + std::to_string(kMaxArgs) + "]; };\n";
-    s += "extern \"C\" __global__ void __launch_bounds__(" + std::to_string(kThreads) +
-         ") fvb_gen(const FvbArgs a, const fvb_u64 n)\n{\n";
+    // 4 consecutive elements per access (the planes may alias: no .nc path)
+    s += "__device__ __forceinline__ void fvb_ld4(const double* p, double* v)\n{\n"
+         "    asm volatile(\"ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\" : \"=d\"(v[0]), "
+         "\"=d\"(v[1]), \"=d\"(v[2]), \"=d\"(v[3]) : \"l\"(p) : \"memory\");\n}\n";
+    s += "__device__ __forceinline__ void fvb_ld4(const float* p, float* v)\n{\n"
+         "    asm volatile(\"ld.global.v4.f32 {%0, %1, %2, %3}, [%4];\" : \"=f\"(v[0]), "
+         "\"=f\"(v[1]), \"=f\"(v[2]), \"=f\"(v[3]) : \"l\"(p) : \"memory\");\n}\n";
+    s += "__device__ __forceinline__ void fvb_st4(double* p, const double* v)\n{\n"
+         "    asm volatile(\"st.global.v4.f64 [%0], {%1, %2, %3, %4};\" :: \"l\"(p), \"d\"(v[0]), "
+         "\"d\"(v[1]), \"d\"(v[2]), \"d\"(v[3]) : \"memory\");\n}\n";
+    s += "__device__ __forceinline__ void fvb_st4(float* p, const float* v)\n{\n"
+         "    asm volatile(\"st.global.v4.f32 [%0], {%1, %2, %3, %4};\" :: \"l\"(p), \"f\"(v[0]), "
+         "\"f\"(v[1]), \"f\"(v[2]), \"f\"(v[3]) : \"memory\");\n}\n";
+    // the tree, once per element
+    s += "__device__ __forceinline__ void fvb_point(";
+    for (int i = 0; i < nin; ++i)
+        s += std::string(i ? ", " : "") + "const " + ctype(d.slot_prec.at(i)) + " l" +
+             std::to_string(i);
+    for (int j = 0; j < nout; ++j)
+        s += std::string(nin || j ? ", " : "") + ctype(d.dest_prec[j]) + "& r" + std::to_string(j);
+    s += ")\n{\n";
+    s += e.body;
+    for (int j = 0; j < nout; ++j)
+        s += "            r" + std::to_string(j) + " = " + roots[j] + ";\n";
+    s += "}\n";
+    auto call = [&](const std::string& leaf_fmt, const std::string& out_fmt) {
+        // fvb_point(<leaf i>, ..., <out j>, ...) with {} replaced by the index
+        std::string c = "fvb_point(";
+        auto sub = [](std::string f, int k) {
+            for (size_t at; (at = f.find("{}")) != std::string::npos;)
+                f.replace(at, 2, std::to_string(k));
+            return f;
+        };
+        for (int i = 0; i < nin; ++i) c += (i ? ", " : "") + sub(leaf_fmt, i);
+        for (int j = 0; j < nout; ++j) c += (nin || j ? ", " : "") + sub(out_fmt, j);
+        return c + ");\n";
+    };
+    s += "extern \"C\" __global__ void __launch_bounds__(" + T + ", " + std::to_string(minb) +
+         ") fvb_gen(const FvbArgs a, const fvb_u64 n, const int vec)\n{\n";
     for (int j = 0; j < nout; ++j)
         s += std::string("    ") + ctype(d.dest_prec[j]) + "* o" + std::to_string(j) + " = (" +
              ctype(d.dest_prec[j]) + "*)a.p[" + std::to_string(j) + "];\n";
@@ -295,17 +335,41 @@ bool emit(const char* key, std::string* src, KDag* dag_out) {
         s += std::string("    const ") + t + "* q" + std::to_string(i) + " = (const " + t +
              "*)a.p[" + std::to_string(nout + i) + "];\n";
     }
-    s += "    const fvb_u64 base = (fvb_u64)blockIdx.x * " + std::to_string(kThreads * kPerThread) +
-         "ull + threadIdx.x;\n";
-    s += "#pragma unroll\n    for (int u = 0; u < " + std::to_string(kPerThread) + "; ++u) {\n";
-    s += "        const fvb_u64 i = base + (fvb_u64)u * " + std::to_string(kThreads) + "ull;\n";
-    s += "        if (i < n) {\n";
+    // every plane 4-element aligned: 4 consecutive elements per thread with
+    // one wide access per plane; all loads, then the tree, then all stores
+    s += "    if (vec) {\n";
+    s += "        const fvb_u64 i0 = ((fvb_u64)blockIdx.x * " + T + "ull + threadIdx.x) * 4ull;\n";
+    s += "        if (i0 + 4ull <= n) {\n";
     for (int i = 0; i < nin; ++i)
-        s += std::string("            const ") + ctype(d.slot_prec.at(i)) + " l" + std::to_string(i) +
-             " = q" + std::to_string(i) + "[i];\n";
-    s += e.body;
+        s += std::string("            ") + ctype(d.slot_prec.at(i)) + " v" + std::to_string(i) +
+             "[4];\n            fvb_ld4(q" + std::to_string(i) + " + i0, v" + std::to_string(i) +
+             ");\n";
     for (int j = 0; j < nout; ++j)
-        s += "            o" + std::to_string(j) + "[i] = " + roots[j] + ";\n";
+        s += std::string("            ") + ctype(d.dest_prec[j]) + " w" + std::to_string(j) +
+             "[4];\n";
+    s += "#pragma unroll\n            for (int k = 0; k < 4; ++k) " + call("v{}[k]", "w{}[k]");
+    for (int j = 0; j < nout; ++j)
+        s += "            fvb_st4(o" + std::to_string(j) + " + i0, w" + std::to_string(j) + ");\n";
+    s += "        } else {\n";
+    s += "            for (fvb_u64 i = i0; i < n; ++i) {\n";
+    for (int j = 0; j < nout; ++j)
+        s += std::string("                ") + ctype(d.dest_prec[j]) + " w" + std::to_string(j) +
+             ";\n";
+    s += "                " + call("q{}[i]", "w{}");
+    for (int j = 0; j < nout; ++j)
+        s += "                o" + std::to_string(j) + "[i] = w" + std::to_string(j) + ";\n";
+    s += "            }\n        }\n        return;\n    }\n";
+    // otherwise element-wide, 4 elements per thread strided by the CTA width
+    s += "    const fvb_u64 base = (fvb_u64)blockIdx.x * " +
+         std::to_string(kThreads * kPerThread) + "ull + threadIdx.x;\n";
+    s += "#pragma unroll\n    for (int u = 0; u < " + std::to_string(kPerThread) + "; ++u) {\n";
+    s += "        const fvb_u64 i = base + (fvb_u64)u * " + T + "ull;\n";
+    s += "        if (i < n) {\n";
+    for (int j = 0; j < nout; ++j)
+        s += std::string("            ") + ctype(d.dest_prec[j]) + " w" + std::to_string(j) + ";\n";
+    s += "            " + call("q{}[i]", "w{}");
+    for (int j = 0; j < nout; ++j)
+        s += "            o" + std::to_string(j) + "[i] = w" + std::to_string(j) + ";\n";
     s += "        }\n    }\n}\n";
     *src = s;
     if (dag_out) *dag_out = std::move(d);
@@ -414,10 +478,16 @@ fvb_status gen_entry(const fvb_kernel* k, uint64_t begin, uint64_t end, void* co
             return fail(FVB_EALIGN, "argument plane is not element-aligned");
         la.p[i] = static_cast<char*>(args[i]) + begin * w;
     }
+    // 4-element accesses when every plane (after the begin offset) allows them
+    int vec = 1;
+    for (uint32_t i = 0; i < g->nout + g->nin; ++i) {
+        const size_t w = g->arg_prec[i] == 's' ? sizeof(float) : sizeof(double);
+        if (reinterpret_cast<uintptr_t>(la.p[i]) % (4 * w)) vec = 0;
+    }
     const uint64_t per = uint64_t(kThreads) * kPerThread;
     const uint64_t grid = (n + per - 1) / per;
     if (grid > 0x7fffffffull) return fail(FVB_EARG, "range too large for one launch");
-    void* params[] = {&la, &n};
+    void* params[] = {&la, &n, &vec};
     const cudaError_t e =
         cudaLaunchKernel(reinterpret_cast<const void*>(g->kernel), dim3(unsigned(grid)),
                          dim3(kThreads), params, 0, static_cast<cudaStream_t>(stream));
