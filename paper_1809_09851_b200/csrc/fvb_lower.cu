@@ -270,7 +270,7 @@ struct Emitter {
     }
 };
 
-bool emit(const char* key, std::string* src, KDag* dag_out) {
+bool emit(const char* key, std::string* src, KDag* dag_out, bool wide = true) {
     KDag d;
     Parser p(key, d);
     if (!p.parse()) return false;
@@ -289,15 +289,29 @@ bool emit(const char* key, std::string* src, KDag* dag_out) {
     s += "typedef unsigned long long fvb_u64;\n";
     s += "struct FvbArgs { void* p[" + std::to_string(kMaxArgs) + "]; };\n";
     // 4 consecutive elements per access (the planes may alias: no .nc path)
-    s += "__device__ __forceinline__ void fvb_ld4(const double* p, double* v)\n{\n"
-         "    asm volatile(\"ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\" : \"=d\"(v[0]), "
-         "\"=d\"(v[1]), \"=d\"(v[2]), \"=d\"(v[3]) : \"l\"(p) : \"memory\");\n}\n";
+    if (wide)  // sm_100's 256-bit access (NVRTC >= 12.9)
+        s += "__device__ __forceinline__ void fvb_ld4(const double* p, double* v)\n{\n"
+             "    asm volatile(\"ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\" : \"=d\"(v[0]), "
+             "\"=d\"(v[1]), \"=d\"(v[2]), \"=d\"(v[3]) : \"l\"(p) : \"memory\");\n}\n";
+    else
+        s += "__device__ __forceinline__ void fvb_ld4(const double* p, double* v)\n{\n"
+             "    asm volatile(\"ld.global.v2.f64 {%0, %1}, [%2];\" : \"=d\"(v[0]), \"=d\"(v[1]) "
+             ": \"l\"(p) : \"memory\");\n"
+             "    asm volatile(\"ld.global.v2.f64 {%0, %1}, [%2];\" : \"=d\"(v[2]), \"=d\"(v[3]) "
+             ": \"l\"(p + 2) : \"memory\");\n}\n";
     s += "__device__ __forceinline__ void fvb_ld4(const float* p, float* v)\n{\n"
          "    asm volatile(\"ld.global.v4.f32 {%0, %1, %2, %3}, [%4];\" : \"=f\"(v[0]), "
          "\"=f\"(v[1]), \"=f\"(v[2]), \"=f\"(v[3]) : \"l\"(p) : \"memory\");\n}\n";
-    s += "__device__ __forceinline__ void fvb_st4(double* p, const double* v)\n{\n"
-         "    asm volatile(\"st.global.v4.f64 [%0], {%1, %2, %3, %4};\" :: \"l\"(p), \"d\"(v[0]), "
-         "\"d\"(v[1]), \"d\"(v[2]), \"d\"(v[3]) : \"memory\");\n}\n";
+    if (wide)
+        s += "__device__ __forceinline__ void fvb_st4(double* p, const double* v)\n{\n"
+             "    asm volatile(\"st.global.v4.f64 [%0], {%1, %2, %3, %4};\" :: \"l\"(p), "
+             "\"d\"(v[0]), \"d\"(v[1]), \"d\"(v[2]), \"d\"(v[3]) : \"memory\");\n}\n";
+    else
+        s += "__device__ __forceinline__ void fvb_st4(double* p, const double* v)\n{\n"
+             "    asm volatile(\"st.global.v2.f64 [%0], {%1, %2};\" :: \"l\"(p), \"d\"(v[0]), "
+             "\"d\"(v[1]) : \"memory\");\n"
+             "    asm volatile(\"st.global.v2.f64 [%0], {%1, %2};\" :: \"l\"(p + 2), \"d\"(v[2]), "
+             "\"d\"(v[3]) : \"memory\");\n}\n";
     s += "__device__ __forceinline__ void fvb_st4(float* p, const float* v)\n{\n"
          "    asm volatile(\"st.global.v4.f32 [%0], {%1, %2, %3, %4};\" :: \"l\"(p), \"f\"(v[0]), "
          "\"f\"(v[1]), \"f\"(v[2]), \"f\"(v[3]) : \"memory\");\n}\n";
@@ -394,8 +408,12 @@ const Nvrtc& nvrtc() {
     static const Nvrtc lib = [] {
         Nvrtc n;
         void* h = nullptr;
-        for (const char* name : {"libnvrtc.so.12", "libnvrtc.so",
-                                 "/usr/local/cuda/lib64/libnvrtc.so.12"}) {
+        // The toolkit's own NVRTC first (the one matching the nvcc that built
+        // this library): a host process may already hold an older
+        // libnvrtc.so.12 (torch bundles one) whose ptxas lacks sm_100a's
+        // 256-bit accesses; an explicit path loads ours beside it.
+        for (const char* name : {FVB_CUDA_LIB64 "/libnvrtc.so.12", "libnvrtc.so.12",
+                                 "libnvrtc.so"}) {
             h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
             if (h) break;
         }
@@ -506,7 +524,10 @@ fvb_status lower_lookup(const char* key, fvb_kernel* out) {
             return fail(FVB_EUNSUPPORTED, std::string("not a loweable structural key: ") +
                                               std::string(key).substr(0, 160));
         std::vector<char> image;
-        if (fvb_status st = compile(src, &image)) return st;
+        if (fvb_status st = compile(src, &image)) {
+            // an NVRTC older than sm_100's 256-bit accesses: 128-bit ones
+            if (!emit(key, &src, &d, false) || compile(src, &image)) return st;
+        }
         auto g = std::make_unique<Gen>();
         g->key = key;
         g->nout = uint32_t(d.roots.size());
@@ -564,7 +585,9 @@ fvb_status fvb_nvrtc_compile(const char* key, size_t* cubin_bytes) {
     if (!emit(key, &src, nullptr))
         return fail(FVB_EUNSUPPORTED, "not a loweable structural key");
     std::vector<char> image;
-    if (fvb_status st = compile(src, &image)) return st;
+    if (fvb_status st = compile(src, &image)) {
+        if (!emit(key, &src, nullptr, false) || compile(src, &image)) return st;
+    }
     if (cubin_bytes) *cubin_bytes = image.size();
     return FVB_OK;
 }

@@ -138,7 +138,7 @@ def test_lowering_emits_the_reference_semantics():
     key = "dB2d(Cd3fb999999999999a;,U15s(Ls0;))"
     src = fvb.emit_source(key)
     assert "sqrtf(l0)" in src and "(0x1.999999999999ap-4)" in src
-    assert "r0 = (double)(t0);" in src and "fvb_st4(o0 + i0, w0);" in src
+    assert "* (double)(t0))" in src and "r0 = t1;" in src and "fvb_st4(o0 + i0, w0);" in src
     # shared subtrees are computed once across block items
     blk = "G2x1:dB2d(Ld0;,Ld1;)|dB0d(B2d(Ld0;,Ld1;),Ld1;)"
     src = fvb.emit_source(blk)
