@@ -24,6 +24,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -270,7 +271,7 @@ struct Emitter {
     }
 };
 
-bool emit(const char* key, std::string* src, KDag* dag_out, bool wide = true) {
+bool emit(const char* key, std::string* src, KDag* dag_out, bool wide = true, int minb = 2) {
     KDag d;
     Parser p(key, d);
     if (!p.parse()) return false;
@@ -281,8 +282,8 @@ bool emit(const char* key, std::string* src, KDag* dag_out, bool wide = true) {
     Emitter e(d);
     std::vector<std::string> roots;
     for (int r : d.roots) roots.push_back(e.as(d.dest_prec[roots.size()], r));
-    // a register cap of 128 (2 CTAs/SM) for trees small enough not to spill
-    const int minb = int(d.nodes.size()) + nout <= 48 ? 2 : 1;
+    // minb = 2: a 128-register cap, 16 warps/SM; build() drops to 1 when the
+    // tree would spill under it
     const std::string T = std::to_string(kThreads);
     std::string s;
     s += "// lowered by libfvb from a structural key (proj/src/backend_jit.cpp grammar)\n";
@@ -435,22 +436,30 @@ const Nvrtc& nvrtc() {
     return lib;
 }
 
-fvb_status compile(const std::string& src, std::vector<char>* image) {
+fvb_status compile(const std::string& src, std::vector<char>* image, bool* spilled) {
     const Nvrtc& nv = nvrtc();
     if (!nv.ok) return fail(FVB_EUNSUPPORTED, "general lowering unavailable: " + nv.why);
     nvrtcProgram prog;
     if (nv.create(&prog, src.c_str(), "fvb_gen.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
         return fail(FVB_EUNSUPPORTED, "nvrtcCreateProgram failed");
     const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--prec-div=true",
-                          "--prec-sqrt=true", "--ftz=false", "--std=c++17", "-default-device"};
+                          "--prec-sqrt=true", "--ftz=false", "--std=c++17", "-default-device",
+                          "--ptxas-options=-v"};
     const nvrtcResult rc = nv.compile(prog, int(sizeof(opts) / sizeof(opts[0])), opts);
+    size_t n = 0;
+    nv.log_size(prog, &n);
+    std::string log(n, '\0');
+    if (n) nv.log(prog, &log[0]);
     if (rc != NVRTC_SUCCESS) {
-        size_t n = 0;
-        nv.log_size(prog, &n);
-        std::string log(n, '\0');
-        if (n) nv.log(prog, &log[0]);
         nv.destroy(&prog);
         return fail(FVB_EUNSUPPORTED, "NVRTC compile failed: " + log.substr(0, 400));
+    }
+    // ptxas -v: "N bytes spill stores"
+    *spilled = false;
+    for (size_t at = 0; (at = log.find(" bytes spill stores", at)) != std::string::npos; ++at) {
+        size_t b = at;
+        while (b > 0 && log[b - 1] >= '0' && log[b - 1] <= '9') --b;
+        if (b < at && std::atol(log.c_str() + b) > 0) *spilled = true;
     }
     size_t bytes = 0;
     nv.cubin_size(prog, &bytes);
@@ -458,6 +467,26 @@ fvb_status compile(const std::string& src, std::vector<char>* image) {
     nv.cubin(prog, image->data());
     nv.destroy(&prog);
     return FVB_OK;
+}
+
+// Emit and compile a key: 256-bit accesses and a 2-CTA/SM register cap
+// first; without the cap when the tree would spill under it; 128-bit
+// accesses when the NVRTC in use predates sm_100's 256-bit ones.
+fvb_status build(const char* key, KDag* d, std::vector<char>* image) {
+    fvb_status last = FVB_EUNSUPPORTED;
+    for (bool wide : {true, false}) {
+        for (int minb : {2, 1}) {
+            std::string src;
+            if (!emit(key, &src, d, wide, minb))
+                return fail(FVB_EUNSUPPORTED, std::string("not a loweable structural key: ") +
+                                                  std::string(key).substr(0, 160));
+            bool spilled = false;
+            last = compile(src, image, &spilled);
+            if (last != FVB_OK) break;  // try the 128-bit form
+            if (!spilled || minb == 1) return FVB_OK;
+        }
+    }
+    return last;
 }
 
 // ---- the per-key cache and the launch entry -----------------------------------
@@ -518,16 +547,9 @@ fvb_status lower_lookup(const char* key, fvb_kernel* out) {
     std::lock_guard<std::mutex> lock(g_mu);
     auto it = cache().find(key);
     if (it == cache().end()) {
-        std::string src;
         KDag d;
-        if (!emit(key, &src, &d))
-            return fail(FVB_EUNSUPPORTED, std::string("not a loweable structural key: ") +
-                                              std::string(key).substr(0, 160));
         std::vector<char> image;
-        if (fvb_status st = compile(src, &image)) {
-            // an NVRTC older than sm_100's 256-bit accesses: 128-bit ones
-            if (!emit(key, &src, &d, false) || compile(src, &image)) return st;
-        }
+        if (fvb_status st = build(key, &d, &image)) return st;
         auto g = std::make_unique<Gen>();
         g->key = key;
         g->nout = uint32_t(d.roots.size());
@@ -581,13 +603,9 @@ fvb_status fvb_emit_source(const char* key, char* buf, size_t cap, size_t* len) 
 
 fvb_status fvb_nvrtc_compile(const char* key, size_t* cubin_bytes) {
     if (!key) return fail(FVB_EARG, "NULL key");
-    std::string src;
-    if (!emit(key, &src, nullptr))
-        return fail(FVB_EUNSUPPORTED, "not a loweable structural key");
+    KDag d;
     std::vector<char> image;
-    if (fvb_status st = compile(src, &image)) {
-        if (!emit(key, &src, nullptr, false) || compile(src, &image)) return st;
-    }
+    if (fvb_status st = build(key, &d, &image)) return st;
     if (cubin_bytes) *cubin_bytes = image.size();
     return FVB_OK;
 }
