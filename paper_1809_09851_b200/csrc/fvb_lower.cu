@@ -26,6 +26,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -215,59 +216,71 @@ std::string literal(double v, char p) {
     return buf;
 }
 
+// Per-element code generator.  Nodes reached from one item only are that
+// item's private subtree and are emitted inside the item's store loop;
+// nodes shared by several items (the block's common subexpressions, e.g.
+// v_j and p of the flux) are computed once per element up front.  This is
+// the hand-written kernels' prepare()/out() split, derived from the DAG, and
+// keeps only the shared state live while outputs stream out.
 struct Emitter {
     const KDag& d;
-    std::vector<std::string> name;  // per node: expression to use
-    std::string body;
-    int temps = 0;
+    std::vector<int> owner;  // item index, or -2 when shared by several items
+    explicit Emitter(const KDag& dag) : d(dag), owner(dag.nodes.size(), -1) {
+        for (size_t j = 0; j < d.roots.size(); ++j) mark(d.roots[j], int(j));
+    }
 
-    explicit Emitter(const KDag& dag) : d(dag), name(dag.nodes.size()) {}
+    void mark(int idx, int item) {
+        int& o = owner[idx];
+        if (o == item || o == -2) return;
+        o = (o == -1) ? item : -2;
+        const KNode& n = d.nodes[idx];
+        if (n.l >= 0) mark(n.l, o == -2 ? -2 : item);
+        if (n.r >= 0) mark(n.r, o == -2 ? -2 : item);
+    }
 
-    std::string as(char want, int idx) {
-        const std::string& e = get(idx);
+    bool computed(int idx) const { return d.nodes[idx].kind == 'U' || d.nodes[idx].kind == 'B'; }
+
+    // Expression naming node idx for element k (inside the k loop).
+    std::string ref(int idx) const {
+        const KNode& n = d.nodes[idx];
+        if (n.kind == 'L') return "v" + std::to_string(n.slot) + "[k]";
+        if (n.kind == 'C') return literal(n.value, n.prec);
+        if (owner[idx] == -2) return "s" + std::to_string(idx) + "[k]";
+        return "p" + std::to_string(idx);
+    }
+
+    std::string as(char want, int idx) const {
+        const std::string e = ref(idx);
         if (d.nodes[idx].prec == want) return e;
         return std::string("(") + ctype(want) + ")(" + e + ")";
     }
 
-    const std::string& get(int idx) {
-        if (!name[idx].empty()) return name[idx];
+    // The operation of a computed node on its children's references.
+    std::string op(int idx) const {
         const KNode& n = d.nodes[idx];
-        std::string expr;
-        switch (n.kind) {
-            case 'L':
-                name[idx] = "l" + std::to_string(n.slot);
-                return name[idx];
-            case 'C':
-                name[idx] = literal(n.value, n.prec);
-                return name[idx];
-            case 'U': {
-                const std::string c = as(n.prec, n.l);
-                if (n.op == 0) {
-                    expr = "(-(" + c + "))";
-                } else {
-                    std::string fn = unary_fn(n.op);
-                    if (n.prec == 's') fn += 'f';
-                    expr = fn + "(" + c + ")";
-                }
-                break;
-            }
-            default: {
-                const std::string a = as(n.prec, n.l);
-                const std::string b = as(n.prec, n.r);
-                if (const char* op = binary_infix(n.op)) {
-                    expr = "(" + a + " " + op + " " + b + ")";
-                } else {
-                    std::string fn = binary_fn(n.op);
-                    if (n.prec == 's') fn += 'f';
-                    expr = fn + "(" + a + ", " + b + ")";
-                }
-                break;
-            }
+        if (n.kind == 'U') {
+            const std::string c = as(n.prec, n.l);
+            if (n.op == 0) return "(-(" + c + "))";
+            std::string fn = unary_fn(n.op);
+            if (n.prec == 's') fn += 'f';
+            return fn + "(" + c + ")";
         }
-        const std::string t = "t" + std::to_string(temps++);
-        body += std::string("            const ") + ctype(n.prec) + " " + t + " = " + expr + ";\n";
-        name[idx] = t;
-        return name[idx];
+        const std::string a = as(n.prec, n.l), b = as(n.prec, n.r);
+        if (const char* o = binary_infix(n.op)) return "(" + a + " " + o + " " + b + ")";
+        std::string fn = binary_fn(n.op);
+        if (n.prec == 's') fn += 'f';
+        return fn + "(" + a + ", " + b + ")";
+    }
+
+    // Post-order emission of the computed nodes selected by `want`.
+    void post(int idx, const std::function<bool(int)>& want, std::vector<bool>& done,
+              std::vector<int>& order) const {
+        if (done[idx]) return;
+        const KNode& n = d.nodes[idx];
+        if (n.l >= 0) post(n.l, want, done, order);
+        if (n.r >= 0) post(n.r, want, done, order);
+        done[idx] = true;
+        if (computed(idx) && want(idx)) order.push_back(idx);
     }
 };
 
@@ -280,112 +293,91 @@ bool emit(const char* key, std::string* src, KDag* dag_out, bool wide = true, in
     if (int(d.slot_prec.size()) != nin) return false;  // slots must be dense 0..nin-1
     if (nout + nin > kMaxArgs) return false;
     Emitter e(d);
-    std::vector<std::string> roots;
-    for (int r : d.roots) roots.push_back(e.as(d.dest_prec[roots.size()], r));
-    // minb = 2: a 128-register cap, 16 warps/SM; build() drops to 1 when the
-    // tree would spill under it
     const std::string T = std::to_string(kThreads);
+    auto num = [](int x) { return std::to_string(x); };
     std::string s;
     s += "// lowered by libfvb from a structural key (proj/src/backend_jit.cpp grammar)\n";
     s += "typedef unsigned long long fvb_u64;\n";
-    s += "struct FvbArgs { void* p[" + std::to_string(kMaxArgs) + "]; };\n";
+    s += "struct FvbArgs { void* p[" + num(kMaxArgs) + "]; };\n";
     // 4 consecutive elements per access (the planes may alias: no .nc path)
     if (wide)  // sm_100's 256-bit access (NVRTC >= 12.9)
         s += "__device__ __forceinline__ void fvb_ld4(const double* p, double* v)\n{\n"
              "    asm volatile(\"ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\" : \"=d\"(v[0]), "
-             "\"=d\"(v[1]), \"=d\"(v[2]), \"=d\"(v[3]) : \"l\"(p) : \"memory\");\n}\n";
+             "\"=d\"(v[1]), \"=d\"(v[2]), \"=d\"(v[3]) : \"l\"(p) : \"memory\");\n}\n"
+             "__device__ __forceinline__ void fvb_st4(double* p, const double* v)\n{\n"
+             "    asm volatile(\"st.global.v4.f64 [%0], {%1, %2, %3, %4};\" :: \"l\"(p), "
+             "\"d\"(v[0]), \"d\"(v[1]), \"d\"(v[2]), \"d\"(v[3]) : \"memory\");\n}\n";
     else
         s += "__device__ __forceinline__ void fvb_ld4(const double* p, double* v)\n{\n"
              "    asm volatile(\"ld.global.v2.f64 {%0, %1}, [%2];\" : \"=d\"(v[0]), \"=d\"(v[1]) "
              ": \"l\"(p) : \"memory\");\n"
              "    asm volatile(\"ld.global.v2.f64 {%0, %1}, [%2];\" : \"=d\"(v[2]), \"=d\"(v[3]) "
-             ": \"l\"(p + 2) : \"memory\");\n}\n";
-    s += "__device__ __forceinline__ void fvb_ld4(const float* p, float* v)\n{\n"
-         "    asm volatile(\"ld.global.v4.f32 {%0, %1, %2, %3}, [%4];\" : \"=f\"(v[0]), "
-         "\"=f\"(v[1]), \"=f\"(v[2]), \"=f\"(v[3]) : \"l\"(p) : \"memory\");\n}\n";
-    if (wide)
-        s += "__device__ __forceinline__ void fvb_st4(double* p, const double* v)\n{\n"
-             "    asm volatile(\"st.global.v4.f64 [%0], {%1, %2, %3, %4};\" :: \"l\"(p), "
-             "\"d\"(v[0]), \"d\"(v[1]), \"d\"(v[2]), \"d\"(v[3]) : \"memory\");\n}\n";
-    else
-        s += "__device__ __forceinline__ void fvb_st4(double* p, const double* v)\n{\n"
+             ": \"l\"(p + 2) : \"memory\");\n}\n"
+             "__device__ __forceinline__ void fvb_st4(double* p, const double* v)\n{\n"
              "    asm volatile(\"st.global.v2.f64 [%0], {%1, %2};\" :: \"l\"(p), \"d\"(v[0]), "
              "\"d\"(v[1]) : \"memory\");\n"
              "    asm volatile(\"st.global.v2.f64 [%0], {%1, %2};\" :: \"l\"(p + 2), \"d\"(v[2]), "
              "\"d\"(v[3]) : \"memory\");\n}\n";
-    s += "__device__ __forceinline__ void fvb_st4(float* p, const float* v)\n{\n"
+    s += "__device__ __forceinline__ void fvb_ld4(const float* p, float* v)\n{\n"
+         "    asm volatile(\"ld.global.v4.f32 {%0, %1, %2, %3}, [%4];\" : \"=f\"(v[0]), "
+         "\"=f\"(v[1]), \"=f\"(v[2]), \"=f\"(v[3]) : \"l\"(p) : \"memory\");\n}\n"
+         "__device__ __forceinline__ void fvb_st4(float* p, const float* v)\n{\n"
          "    asm volatile(\"st.global.v4.f32 [%0], {%1, %2, %3, %4};\" :: \"l\"(p), \"f\"(v[0]), "
          "\"f\"(v[1]), \"f\"(v[2]), \"f\"(v[3]) : \"memory\");\n}\n";
-    // the tree, once per element
-    s += "__device__ __forceinline__ void fvb_point(";
-    for (int i = 0; i < nin; ++i)
-        s += std::string(i ? ", " : "") + "const " + ctype(d.slot_prec.at(i)) + " l" +
-             std::to_string(i);
-    for (int j = 0; j < nout; ++j)
-        s += std::string(nin || j ? ", " : "") + ctype(d.dest_prec[j]) + "& r" + std::to_string(j);
-    s += ")\n{\n";
-    s += e.body;
-    for (int j = 0; j < nout; ++j)
-        s += "            r" + std::to_string(j) + " = " + roots[j] + ";\n";
-    s += "}\n";
-    auto call = [&](const std::string& leaf_fmt, const std::string& out_fmt) {
-        // fvb_point(<leaf i>, ..., <out j>, ...) with {} replaced by the index
-        std::string c = "fvb_point(";
-        auto sub = [](std::string f, int k) {
-            for (size_t at; (at = f.find("{}")) != std::string::npos;)
-                f.replace(at, 2, std::to_string(k));
-            return f;
-        };
-        for (int i = 0; i < nin; ++i) c += (i ? ", " : "") + sub(leaf_fmt, i);
-        for (int j = 0; j < nout; ++j) c += (nin || j ? ", " : "") + sub(out_fmt, j);
-        return c + ");\n";
-    };
-    s += "extern \"C\" __global__ void __launch_bounds__(" + T + ", " + std::to_string(minb) +
-         ") fvb_gen(const FvbArgs a, const fvb_u64 n, const int vec)\n{\n";
-    for (int j = 0; j < nout; ++j)
-        s += std::string("    ") + ctype(d.dest_prec[j]) + "* o" + std::to_string(j) + " = (" +
-             ctype(d.dest_prec[j]) + "*)a.p[" + std::to_string(j) + "];\n";
+
+    // fvb_tile<E>: E consecutive elements from i0 (E = 4 wide, E = 1 scalar)
+    s += "template <int E>\n__device__ __forceinline__ void fvb_tile(const FvbArgs& a, "
+         "const fvb_u64 i0)\n{\n";
     for (int i = 0; i < nin; ++i) {
         const char* t = ctype(d.slot_prec.at(i));
-        s += std::string("    const ") + t + "* q" + std::to_string(i) + " = (const " + t +
-             "*)a.p[" + std::to_string(nout + i) + "];\n";
+        const std::string q = std::string("((const ") + t + "*)a.p[" + num(nout + i) + "])";
+        s += std::string("    ") + t + " v" + num(i) + "[E];\n";
+        s += "    if constexpr (E == 4) fvb_ld4(" + q + " + i0, v" + num(i) + ");\n";
+        s += "    else v" + num(i) + "[0] = " + q + "[i0];\n";
     }
+    // shared subexpressions, once per element
+    std::vector<bool> done(d.nodes.size(), false);
+    std::vector<int> shared;
+    for (int r : d.roots) e.post(r, [&](int x) { return e.owner[x] == -2; }, done, shared);
+    for (int idx : shared)
+        s += std::string("    ") + ctype(d.nodes[idx].prec) + " s" + num(idx) + "[E];\n";
+    if (!shared.empty()) {
+        s += "#pragma unroll\n    for (int k = 0; k < E; ++k) {\n";
+        for (int idx : shared) s += "        s" + num(idx) + "[k] = " + e.op(idx) + ";\n";
+        s += "    }\n";
+    }
+    // each item: its private subtree, then the store
+    for (int j = 0; j < nout; ++j) {
+        const char* t = ctype(d.dest_prec[j]);
+        const std::string o = std::string("((") + t + "*)a.p[" + num(j) + "])";
+        s += "    {\n        " + std::string(t) + " w[E];\n";
+        s += "#pragma unroll\n        for (int k = 0; k < E; ++k) {\n";
+        std::vector<bool> seen(d.nodes.size(), false);
+        std::vector<int> priv;
+        e.post(d.roots[j], [&](int x) { return e.owner[x] == j; }, seen, priv);
+        for (int idx : priv)
+            s += std::string("            const ") + ctype(d.nodes[idx].prec) + " p" + num(idx) +
+                 " = " + e.op(idx) + ";\n";
+        s += "            w[k] = " + e.as(d.dest_prec[j], d.roots[j]) + ";\n        }\n";
+        s += "        if constexpr (E == 4) fvb_st4(" + o + " + i0, w);\n";
+        s += "        else " + o + "[i0] = w[0];\n    }\n";
+    }
+    s += "}\n";
+
+    s += "extern \"C\" __global__ void __launch_bounds__(" + T + ", " + num(minb) +
+         ") fvb_gen(const FvbArgs a, const fvb_u64 n, const int vec)\n{\n";
     // every plane 4-element aligned: 4 consecutive elements per thread with
-    // one wide access per plane; all loads, then the tree, then all stores
+    // one wide access per plane; otherwise 4 elements strided by the CTA
     s += "    if (vec) {\n";
     s += "        const fvb_u64 i0 = ((fvb_u64)blockIdx.x * " + T + "ull + threadIdx.x) * 4ull;\n";
-    s += "        if (i0 + 4ull <= n) {\n";
-    for (int i = 0; i < nin; ++i)
-        s += std::string("            ") + ctype(d.slot_prec.at(i)) + " v" + std::to_string(i) +
-             "[4];\n            fvb_ld4(q" + std::to_string(i) + " + i0, v" + std::to_string(i) +
-             ");\n";
-    for (int j = 0; j < nout; ++j)
-        s += std::string("            ") + ctype(d.dest_prec[j]) + " w" + std::to_string(j) +
-             "[4];\n";
-    s += "#pragma unroll\n            for (int k = 0; k < 4; ++k) " + call("v{}[k]", "w{}[k]");
-    for (int j = 0; j < nout; ++j)
-        s += "            fvb_st4(o" + std::to_string(j) + " + i0, w" + std::to_string(j) + ");\n";
-    s += "        } else {\n";
-    s += "            for (fvb_u64 i = i0; i < n; ++i) {\n";
-    for (int j = 0; j < nout; ++j)
-        s += std::string("                ") + ctype(d.dest_prec[j]) + " w" + std::to_string(j) +
-             ";\n";
-    s += "                " + call("q{}[i]", "w{}");
-    for (int j = 0; j < nout; ++j)
-        s += "                o" + std::to_string(j) + "[i] = w" + std::to_string(j) + ";\n";
-    s += "            }\n        }\n        return;\n    }\n";
-    // otherwise element-wide, 4 elements per thread strided by the CTA width
-    s += "    const fvb_u64 base = (fvb_u64)blockIdx.x * " +
-         std::to_string(kThreads * kPerThread) + "ull + threadIdx.x;\n";
-    s += "#pragma unroll\n    for (int u = 0; u < " + std::to_string(kPerThread) + "; ++u) {\n";
+    s += "        if (i0 + 4ull <= n) {\n            fvb_tile<4>(a, i0);\n            return;\n"
+         "        }\n";
+    s += "        for (fvb_u64 i = i0; i < n; ++i) fvb_tile<1>(a, i);\n        return;\n    }\n";
+    s += "    const fvb_u64 base = (fvb_u64)blockIdx.x * " + num(kThreads * kPerThread) +
+         "ull + threadIdx.x;\n";
+    s += "#pragma unroll\n    for (int u = 0; u < " + num(kPerThread) + "; ++u) {\n";
     s += "        const fvb_u64 i = base + (fvb_u64)u * " + T + "ull;\n";
-    s += "        if (i < n) {\n";
-    for (int j = 0; j < nout; ++j)
-        s += std::string("            ") + ctype(d.dest_prec[j]) + " w" + std::to_string(j) + ";\n";
-    s += "            " + call("q{}[i]", "w{}");
-    for (int j = 0; j < nout; ++j)
-        s += "            o" + std::to_string(j) + "[i] = w" + std::to_string(j) + ";\n";
-    s += "        }\n    }\n}\n";
+    s += "        if (i < n) fvb_tile<1>(a, i);\n    }\n}\n";
     *src = s;
     if (dag_out) *dag_out = std::move(d);
     return true;

@@ -127,8 +127,8 @@ def test_near_misses_do_not_hit_the_hand_written_kernel():
     # well-formed keys that differ from the axpy pattern are lowered, never
     # silently run as axpy-sin: their source is the tree they describe
     for key, needle in [(axpy_key().replace("U2d", "U3d"), "cos("),
-                        (axpy_key().replace("Ld1;", "Ld0;"), "(l0 + l0)"),
-                        ("s" + axpy_key()[1:], "r0 = (float)(")]:
+                        (axpy_key().replace("Ld1;", "Ld0;"), "(v0[k] + v0[k])"),
+                        ("s" + axpy_key()[1:], "w[k] = (float)(")]:
         src = fvb.emit_source(key)
         assert needle in src, src
 
@@ -137,12 +137,13 @@ def test_lowering_emits_the_reference_semantics():
     # sqrt in f32 on an f32 leaf, promoted to f64 for the product, hex constant
     key = "dB2d(Cd3fb999999999999a;,U15s(Ls0;))"
     src = fvb.emit_source(key)
-    assert "sqrtf(l0)" in src and "(0x1.999999999999ap-4)" in src
-    assert "* (double)(t0))" in src and "r0 = t1;" in src and "fvb_st4(o0 + i0, w0);" in src
+    assert "sqrtf(v0[k])" in src and "(0x1.999999999999ap-4)" in src
+    assert "* (double)(p" in src and "fvb_st4(((double*)a.p[0]) + i0, w);" in src
     # shared subtrees are computed once across block items
     blk = "G2x1:dB2d(Ld0;,Ld1;)|dB0d(B2d(Ld0;,Ld1;),Ld1;)"
     src = fvb.emit_source(blk)
-    assert src.count("(l0 * l1)") == 1
+    assert src.count("(v0[k] * v1[k])") == 1
+    assert re.search(r"s\d+\[k\] = \(v0\[k\] \* v1\[k\]\);", src)
 
 
 def test_lowered_kernels_compile_with_nvrtc():
