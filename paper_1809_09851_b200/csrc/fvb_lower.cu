@@ -464,10 +464,17 @@ fvb_status compile(const std::string& src, std::vector<char>* image, bool* spill
 // Emit and compile a key: 256-bit accesses and a 2-CTA/SM register cap
 // first; without the cap when the tree would spill under it; 128-bit
 // accesses when the NVRTC in use predates sm_100's 256-bit ones.
-fvb_status build(const char* key, KDag* d, std::vector<char>* image) {
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
+
+fvb_status build(const char* key, KDag* d, std::vector<char>* image, int* minb_out) {
     fvb_status last = FVB_EUNSUPPORTED;
+    const int forced = env_int("FVB_LOWER_MINB", 0);  // tuning experiments only
     for (bool wide : {true, false}) {
         for (int minb : {2, 1}) {
+            if (forced && minb != forced) continue;
             std::string src;
             if (!emit(key, &src, d, wide, minb))
                 return fail(FVB_EUNSUPPORTED, std::string("not a loweable structural key: ") +
@@ -475,7 +482,8 @@ fvb_status build(const char* key, KDag* d, std::vector<char>* image) {
             bool spilled = false;
             last = compile(src, image, &spilled);
             if (last != FVB_OK) break;  // try the 128-bit form
-            if (!spilled || minb == 1) return FVB_OK;
+            *minb_out = minb;
+            if (!spilled || minb == 1 || forced) return FVB_OK;
         }
     }
     return last;
@@ -489,6 +497,7 @@ struct Gen {
     cudaKernel_t kernel = nullptr;
     std::vector<char> arg_prec;  // 's'/'d' per argument slot (outputs, then leaves)
     uint32_t nout = 0, nin = 0;
+    int minb = 2;                // resident CTAs per SM the kernel was compiled for
 };
 
 std::mutex g_mu;
@@ -518,7 +527,8 @@ fvb_status gen_entry(const fvb_kernel* k, uint64_t begin, uint64_t end, void* co
         la.p[i] = static_cast<char*>(args[i]) + begin * w;
     }
     // 4-element accesses when every plane (after the begin offset) allows them
-    int vec = 1;
+    static const int allow_vec = env_int("FVB_LOWER_VEC", 1);
+    int vec = allow_vec;
     for (uint32_t i = 0; i < g->nout + g->nin; ++i) {
         const size_t w = g->arg_prec[i] == 's' ? sizeof(float) : sizeof(double);
         if (reinterpret_cast<uintptr_t>(la.p[i]) % (4 * w)) vec = 0;
@@ -541,8 +551,10 @@ fvb_status lower_lookup(const char* key, fvb_kernel* out) {
     if (it == cache().end()) {
         KDag d;
         std::vector<char> image;
-        if (fvb_status st = build(key, &d, &image)) return st;
+        int minb = 2;
+        if (fvb_status st = build(key, &d, &image, &minb)) return st;
         auto g = std::make_unique<Gen>();
+        g->minb = minb;
         g->key = key;
         g->nout = uint32_t(d.roots.size());
         g->nin = uint32_t(d.slot_prec.size());
@@ -567,7 +579,8 @@ fvb_status lower_lookup(const char* key, fvb_kernel* out) {
     // A lowered kernel has no canonical input order: it takes its leaves in
     // the key's slot order, which is exactly the jit_args order.
     for (int i = 0; i < 8; ++i) k.in_slot[i] = -1;
-    std::snprintf(k.name, sizeof k.name, "gen:%016zx", std::hash<std::string>()(g->key));
+    std::snprintf(k.name, sizeof k.name, "gen:%016zx:m%d", std::hash<std::string>()(g->key),
+                  g->minb);
     k.impl = g;
     *out = k;
     return FVB_OK;
@@ -597,7 +610,8 @@ fvb_status fvb_nvrtc_compile(const char* key, size_t* cubin_bytes) {
     if (!key) return fail(FVB_EARG, "NULL key");
     KDag d;
     std::vector<char> image;
-    if (fvb_status st = build(key, &d, &image)) return st;
+    int minb = 2;
+    if (fvb_status st = build(key, &d, &image, &minb)) return st;
     if (cubin_bytes) *cubin_bytes = image.size();
     return FVB_OK;
 }
