@@ -481,6 +481,10 @@ fvb_status build(const char* key, KDag* d, std::vector<char>* image, int* minb_o
                                                   std::string(key).substr(0, 160));
             bool spilled = false;
             last = compile(src, image, &spilled);
+            if (env_int("FVB_LOWER_DEBUG", 0))
+                std::fprintf(stderr, "[fvb lower] %016zx wide=%d minb=%d status=%d spilled=%d %s\n",
+                             std::hash<std::string>()(key), int(wide), minb, int(last),
+                             int(spilled), last ? fvb_last_error() : "");
             if (last != FVB_OK) break;  // try the 128-bit form
             *minb_out = minb;
             if (!spilled || minb == 1 || forced) return FVB_OK;
