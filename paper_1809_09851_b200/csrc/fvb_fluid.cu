@@ -17,11 +17,11 @@ fvb_status fvb_axpy_sin(uint8_t prec, uint64_t n, const void* x, void* y, void* 
     if (prec == FVB_F64) {
         const double* in[2] = {static_cast<const double*>(x), static_cast<const double*>(y)};
         double* out[1] = {static_cast<double*>(y)};
-        return launch_op<AxpySinOp<double>, double, false, false>(in, out, n, make_consts<double>(nullptr), nullptr, s);
+        return launch_op<AxpySinOp<double>, double, false, true>(in, out, n, make_consts<double>(nullptr), nullptr, s);
     }
     const float* in[2] = {static_cast<const float*>(x), static_cast<const float*>(y)};
     float* out[1] = {static_cast<float*>(y)};
-    return launch_op<AxpySinOp<float>, float, false, false>(in, out, n, make_consts<float>(nullptr), nullptr, s);
+    return launch_op<AxpySinOp<float>, float, false, true>(in, out, n, make_consts<float>(nullptr), nullptr, s);
 }
 
 fvb_status fvb_cons2prim(const fvb_gas* gas, uint32_t dim, uint8_t prec, uint64_t n,

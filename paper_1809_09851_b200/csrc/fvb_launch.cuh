@@ -166,6 +166,10 @@ fvb_status launch_op(const T* const* in, T* const* out, uint64_t n, const Consts
         FVB_TRY(VD, 1, 512, 1, kTiles)
         FVB_TRY(VD / 2, 2, 256, 1, kTiles)
         FVB_TRY(VD / 2, 4, 256, 1, kTiles)
+        FVB_TRY(VD / 2, 1, 256, 2, kTiles)
+        FVB_TRY(1, 1, 256, 2, kTiles)
+        FVB_TRY(VD / 2, 1, 128, 2, kTiles)
+        FVB_TRY(VD, 1, 128, 2, kTiles)
         FVB_TRY(VD, 1, 256, 1, kPersistent)
         FVB_TRY(VD, 2, 256, 1, kPersistent)
 #undef FVB_TRY
