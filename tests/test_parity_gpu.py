@@ -422,3 +422,32 @@ def test_cons2prim_1e8_sampled_and_round_trip(cuda, orc):
         assert same_bits(got[:, k], want), int(i)
     del s, c, back
     torch.cuda.empty_cache()
+
+
+def test_beyond_32bit_indices(cuda, orc):
+    # Maximum sizes: 2^32 + 4099 points (f32 d=1, 69 GB of planes), so element
+    # indices, vector groups and the generator's global index all pass 2^32.
+    # Points sampled around 2^31 and 2^32 and at the end equal the oracle bit
+    # for bit, and the fused maximum is the max over every per-point lambda.
+    dim, n = 1, (1 << 32) + 4099
+    need = 4 * n * 4 + (2 << 30)
+    if torch.cuda.mem_get_info()[0] < need:
+        pytest.skip("needs ~71 GB of free device memory")
+    s = fvb.synth_state(dim, n, prec=0, seed=0x5EED)
+    lam_pts = torch.empty_like(s[0])
+    _, lam = fvb.wave_speed_max(s, dim, lam_out=lam_pts)
+    torch.cuda.synchronize()
+    assert lam.item() == lam_pts.max().item()
+    idx = np.unique(np.concatenate([
+        np.arange(0, 64), np.arange((1 << 31) - 64, (1 << 31) + 64),
+        np.arange((1 << 32) - 64, (1 << 32) + 64), np.arange(n - 64, n),
+        np.random.default_rng(3).integers(0, n, 200)]))
+    it = torch.from_numpy(idx).to(cuda)
+    got_state = np.stack([t[it].cpu().numpy() for t in s])
+    got_lam = lam_pts[it].cpu().numpy()
+    for k, i in enumerate(idx):
+        pt = orc.random_state(dim, 1, seed=0x5EED, first=int(i), prec="f32")
+        assert same_bits(got_state[:, k], np.array([a[0] for a in pt], np.float32)), int(i)
+        assert np.float32(orc.wave_speed_max(dim, pt)).tobytes() == got_lam[k].tobytes(), int(i)
+    del s, lam_pts
+    torch.cuda.empty_cache()
