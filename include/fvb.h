@@ -41,10 +41,18 @@
  *   - Device entry points take DEVICE pointers and enqueue on `stream`
  *     (a cudaStream_t; NULL = the legacy default stream).  They never
  *     synchronise.  n == 0 is a no-op that returns FVB_OK.
- *   - Outputs must not alias inputs (the reference's sequential item loop
- *     gives order-dependent results for aliased block destinations; see
- *     DESIGN.md).  fvb_axpy_sin is the documented exception: y is in/out,
- *     exactly as the reference allows dest to alias a leaf (backend.hpp:44-46).
+ *   - Aliasing.  The named entry points (fvb_flux, fvb_cons2prim, ...)
+ *     reject, with FVB_EARG before any launch, an output plane that is an
+ *     input plane; fvb_axpy_sin is the exception (y is in/out, as the
+ *     reference lets dest alias a leaf, backend.hpp:44-46).  Kernels from
+ *     fvb_lookup accept an output that IS a leaf plane (in-place evaluation,
+ *     as JitKernel::Fn does) and then read with coherent loads.  A block
+ *     kernel computes every item from the planes as they were at launch; the
+ *     reference's item-by-item loop (block.cpp:413-451) differs only when an
+ *     item reads a plane an earlier item writes, and the C++ adapter
+ *     evaluates such blocks item by item.  Every entry point rejects planes
+ *     that overlap at an offset.  Two outputs may name one plane: the later
+ *     item's value is stored last.
  *   - Results are bitwise identical to the reference for +,-,*,/,sqrt;
  *     sin differs by at most CUDA's 2-ulp bound from glibc's.
  */

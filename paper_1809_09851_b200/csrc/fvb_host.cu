@@ -111,6 +111,12 @@ fvb_status pipeline(fvb_ctx* ctx, const void* const* in, void* const* out, uint6
         if (!in[i]) return fail(FVB_EARG, "NULL input plane");
     for (int j = 0; j < NOUT; ++j)
         if (!out[j]) return fail(FVB_EARG, "NULL output plane");
+    // The chunks of different slots read and write concurrently, and the
+    // pass-through threads copy host-side: host outputs must be disjoint
+    // from the inputs.
+    if (plane_overlap(in, NIN, const_cast<const void* const*>(out), NOUT, size_t(n) * sizeof(T)) !=
+        kDisjoint)
+        return fail(FVB_EARG, "host output plane overlaps an input plane");
     DeviceGuard guard(ctx->device);
     using Bu = typename Bits<T>::U;
     if (RED) {

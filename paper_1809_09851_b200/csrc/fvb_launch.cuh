@@ -88,6 +88,42 @@ bool plan_range(const void* const* ptrs, int count, uint64_t n, Range* rg) {
     return true;
 }
 
+// How the output planes of one launch overlap the planes it reads:
+// kDisjoint, kSame (an output is exactly an input plane: in-place evaluation,
+// as the reference allows for a destination that is also a leaf) or
+// kPartial (overlapping but offset ranges: element i would read what element
+// j != i writes, which no element-wise evaluation order defines).  Outputs
+// that are the same plane are allowed (the later item's store wins, as in
+// the reference's item order); inputs may overlap each other freely.
+enum Overlap { kDisjoint = 0, kSame = 1, kPartial = 2 };
+
+inline Overlap plane_overlap(const void* const* in, int nin, const void* const* out, int nout,
+                             size_t bytes) {
+    auto lo = [](const void* p) { return reinterpret_cast<uintptr_t>(p); };
+    Overlap r = kDisjoint;
+    for (int j = 0; j < nout; ++j) {
+        const uintptr_t o = lo(out[j]);
+        for (int i = 0; i < nin + j; ++i) {
+            const uintptr_t a = i < nin ? lo(in[i]) : lo(out[i - nin]);
+            if (a == o) {
+                if (i < nin) r = kSame;
+            } else if (a < o + bytes && o < a + bytes) {
+                return kPartial;
+            }
+        }
+    }
+    return r;
+}
+
+// An op whose output may be one of its input planes: inputs are read with
+// coherent loads (the non-coherent path assumes memory no thread writes
+// during the kernel).  Each element is still read before it is written by
+// the one thread that owns it.
+template <class Op>
+struct InPlace : Op {
+    static constexpr bool ALIASED = true;
+};
+
 template <class Op, class T, int V, int U, int SP, bool RED, int THREADS = 256, int MINB = 1,
           int MODE = kTiles>
 fvb_status launch_fixed(const Planes<T, Op::NIN, Op::NOUT>& pl, const Consts<T>& k,
@@ -138,6 +174,18 @@ fvb_status launch_op(const T* const* in, T* const* out, uint64_t n, const Consts
         ptrs[np++] = out[j];
     }
     if (Op::NOUT == 0) pl.out[0] = nullptr;
+    switch (plane_overlap(ptrs, Op::NIN, ptrs + Op::NIN, Op::NOUT, size_t(n) * sizeof(T))) {
+        case kPartial:
+            return fail(FVB_EARG, "output plane partially overlaps another plane");
+        case kSame:
+            if (!Op::ALIASED)
+                return fail(FVB_EARG,
+                            "output plane is an input plane: in-place evaluation goes through "
+                            "fvb_lookup kernels");
+            break;
+        default:
+            break;
+    }
 
     constexpr int VD = vec32<T>();
     const Tuning& t = tuning();

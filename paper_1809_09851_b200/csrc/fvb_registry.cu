@@ -292,6 +292,14 @@ fvb_status entry(const fvb_kernel* k, uint64_t begin, uint64_t end, void* const*
         if (!args[j]) return fail(FVB_EARG, "NULL output slot");
         out[j] = static_cast<T*>(args[j]) + begin;
     }
+    // A destination that is also a leaf (evaluate in place, as the
+    // reference's JitKernel allows) runs the coherent-load variant.
+    if (!Op::ALIASED && end > begin &&
+        plane_overlap(reinterpret_cast<const void* const*>(in), Op::NIN,
+                      reinterpret_cast<const void* const*>(out), Op::NOUT,
+                      size_t(end - begin) * sizeof(T)) == kSame)
+        return launch_op<InPlace<Op>, T, false, false>(in, out, end - begin, consts_of<T>(k),
+                                                       nullptr, static_cast<cudaStream_t>(stream));
     return launch_op<Op, T, false, false>(in, out, end - begin, consts_of<T>(k), nullptr,
                                           static_cast<cudaStream_t>(stream));
 }
@@ -314,8 +322,14 @@ fvb_status entry_reduce(const fvb_kernel* k, uint64_t begin, uint64_t end, void*
         if (!args[j]) return fail(FVB_EARG, "NULL output slot");
         out[j] = static_cast<T*>(args[j]) + begin;
     }
-    return launch_op<Op, T, true, false>(in, out, end - begin, consts_of<T>(k),
-                                         static_cast<typename Bits<T>::U*>(red),
+    auto* r = static_cast<typename Bits<T>::U*>(red);
+    if (!Op::ALIASED && end > begin &&
+        plane_overlap(reinterpret_cast<const void* const*>(in), Op::NIN,
+                      reinterpret_cast<const void* const*>(out), Op::NOUT,
+                      size_t(end - begin) * sizeof(T)) == kSame)
+        return launch_op<InPlace<Op>, T, true, false>(in, out, end - begin, consts_of<T>(k), r,
+                                                      static_cast<cudaStream_t>(stream));
+    return launch_op<Op, T, true, false>(in, out, end - begin, consts_of<T>(k), r,
                                          static_cast<cudaStream_t>(stream));
 }
 

@@ -484,6 +484,46 @@ void run_matvec(const DeviceBackend& be, std::vector<std::pair<const BlockItem*,
     }
 }
 
+void leaves_of(const ExprNode& n, std::vector<const DenseVector*>& out) {
+    switch (n.kind) {
+        case NodeKind::Leaf: out.push_back(n.vec); return;
+        case NodeKind::Constant: return;
+        case NodeKind::Tagged:
+        case NodeKind::Cached:
+        case NodeKind::Unary: leaves_of(*n.left, out); return;
+        case NodeKind::Binary:
+            leaves_of(*n.left, out);
+            leaves_of(*n.right, out);
+            return;
+    }
+}
+
+// Does destination o name the storage leaf l reads?  A host destination is
+// the leaf itself; a device one is the leaf's resident copy.
+bool writes_leaf(const DeviceBackend& be, const Out& o, const DenseVector* l) {
+    if (o.host) return o.host == l;
+    return o.dev && be.residency && be.residency->find(l) == o.dev;
+}
+
+// True when some element-wise item reads a vector that an earlier item of
+// the block writes (or that a matvec row writes: those run first here).
+bool reads_earlier_destination(const DeviceBackend& be, const std::vector<Expr>& items,
+                               const std::vector<Out>& outs,
+                               const std::vector<std::pair<const BlockItem*, Out>>& matvecs) {
+    std::vector<const DenseVector*> ls;
+    for (std::size_t k = 0; k < items.size(); ++k) {
+        ls.clear();
+        leaves_of(items[k].node(), ls);
+        for (const DenseVector* l : ls) {
+            for (std::size_t j = 0; j < k; ++j)
+                if (writes_leaf(be, outs[j], l)) return true;
+            for (const auto& mv : matvecs)
+                if (writes_leaf(be, mv.second, l)) return true;
+        }
+    }
+    return false;
+}
+
 // Shared body of the evaluate_block overloads.
 void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, std::size_t cols,
                 const std::vector<Out>& dests_in, void* red, bool need_reduce) {
@@ -518,17 +558,35 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
             items.push_back(x);
             outs.push_back(d);
         }
+    // The reference writes items one by one (block.cpp:413-451), so an item
+    // reading a vector an earlier item of the same block wrote sees the new
+    // values; one fused pass reads every operand before writing anything.
+    // Such blocks are evaluated item by item instead, in the reference's order.
+    const bool hazard = reads_earlier_destination(be, items, outs, matvecs);
+    if (hazard && (need_reduce || !matvecs.empty()))
+        throw UnsupportedExpression(
+            "block whose destinations alias operands of its own items (CFL or matvec block)");
     // Matvec rows first: their operands are captured before any destination
     // of this block is written (the reference's scratch pass, block.cpp:389-411).
     if (!matvecs.empty()) run_matvec(be, matvecs);
     if (items.empty()) return;
-    if (!matvecs.empty()) {  // the fused key covers only the element-wise items
-        rows = items.size();
-        cols = 1;
-    }
     const std::size_t n = outs[0].size();
     for (const Out& o : outs)
         if (o.size() != n) throw LengthMismatch("block destinations have different lengths");
+    if (hazard) {
+        for (std::size_t i = 0; i < items.size(); ++i) {
+            Plan one;
+            if (!try_plan({items[i]}, {outs[i]}, 1, 1, &one)) unsupported({items[i]});
+            run(be, one, n, nullptr);
+        }
+        return;
+    }
+    // Matvec rows or aliased pass-throughs were taken out: the fused key
+    // covers the remaining element-wise items as one column.
+    if (items.size() != rows * cols) {
+        rows = items.size();
+        cols = 1;
+    }
     // Prefer a hand-written fused kernel: the whole block, else the block
     // without its bare-leaf items (plain copies, e.g. the density that
     // convert() passes through).  Only if neither exists, lower the whole

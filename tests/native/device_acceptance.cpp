@@ -598,6 +598,80 @@ void run_gpu() {
         return "";
     });
 
+    check("aliased pass-through: flux into a grid whose row 0 is the momentum fields", [&] {
+        // proj/src/block.cpp:419-422 skips an item whose destination is its
+        // own bare leaf; the remaining items are still fused into one pass.
+        SplitMix64 rng(0xA1);
+        for (std::size_t d = 1; d <= 3; ++d) {
+            const std::size_t n = 20000;
+            auto f = random_state(d, n, rng);
+            auto over = [&](BlockVectorGrid& g) {
+                std::vector<Expr> lv{leaf(f[0])};
+                for (std::size_t j = 0; j < d; ++j) {
+                    g.item(0, j) = f[1 + j];
+                    lv.push_back(leaf(g.item(0, j)));
+                }
+                lv.push_back(leaf(f[d + 1]));
+                return state_conservative(EosSpec(), d, lv);
+            };
+            BlockVectorGrid want(d + 2, d, Precision::f64, n), got(d + 2, d, Precision::f64, n);
+            StateSet uw = over(want), ug = over(got);
+            evaluate_block(ref, inviscid_flux(uw), want);
+            dev::evaluate_block(be, inviscid_flux(ug), got);
+            for (std::size_t i = 0; i < (d + 2) * d; ++i)
+                if (!same_bits(want.get(i), got.get(i)))
+                    fail("d=" + std::to_string(d) + " item " + std::to_string(i));
+        }
+        return "";
+    });
+
+    check("in-place blocks keep the reference's item order (convert over its own state)", [&] {
+        // Item 1 overwrites m with v; the pressure item after it then reads v
+        // in the reference's item-by-item loop.  The device path detects the
+        // hazard and evaluates item by item too.
+        SplitMix64 rng(0xB2);
+        std::size_t differs = 0;
+        for (std::size_t d = 1; d <= 3; ++d) {
+            const std::size_t n = 5000;
+            auto f = random_state(d, n, rng);
+            BlockColVector want{std::vector<DenseVector>(f)}, got{std::vector<DenseVector>(f)};
+            auto over = [&](BlockColVector& v) {
+                std::vector<Expr> lv;
+                for (std::size_t i = 0; i < d + 2; ++i) lv.push_back(leaf(v.get(i)));
+                return state_conservative(EosSpec(), d, lv);
+            };
+            StateSet uw = over(want), ug = over(got);
+            evaluate_block(ref, convert(uw, Formulation::Primitive).block(), want);
+            dev::evaluate_block(be, convert(ug, Formulation::Primitive).block(), got);
+            for (std::size_t i = 0; i < d + 2; ++i)
+                if (!same_bits(want.get(i), got.get(i)))
+                    fail("d=" + std::to_string(d) + " field " + std::to_string(i));
+            // the hazard is real: out of place, p differs
+            StateSet u0 = state_conservative(EosSpec(), d, leaves_of(f));
+            DenseVector p0(Precision::f64, n);
+            StateSet w0 = convert(u0, Formulation::Primitive);
+            evaluate(ref, w0.field(d + 1), p0);
+            if (!same_bits(p0, want.get(d + 1))) ++differs;
+        }
+        if (differs != 3) fail("in-place and out-of-place results coincide");
+        return "";
+    });
+
+    check("in place through a hand-written kernel: pressure into rhoE (d=3)", [&] {
+        SplitMix64 rng(0xC3);
+        const std::size_t n = 70000;
+        auto f = random_state(3, n, rng);
+        auto g = f;
+        StateSet uf = state_conservative(EosSpec(), 3, leaves_of(f));
+        StateSet ug = state_conservative(EosSpec(), 3, leaves_of(g));
+        const std::string name =
+            lookup_name(dev::structural_key(derived_p(ug), Precision::f64));
+        evaluate(ref, derived_p(uf), f[4]);
+        dev::evaluate(be, derived_p(ug), g[4]);
+        if (!same_bits(f[4], g[4])) fail("in-place pressure differs");
+        return "kernel " + name;
+    });
+
     check("errors: unsupported expression, length mismatch, shape mismatch", [&] {
         DenseVector a(Precision::f64, 10), b(Precision::f64, 11), out(Precision::f64, 10);
         bool threw = false;

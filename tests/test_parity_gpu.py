@@ -359,6 +359,47 @@ def test_lookup_kernel_launch(cuda, orc):
     assert names  # canonical order documented in fvb_registry.cu
 
 
+def test_in_place_rules(cuda, orc):
+    import re
+    import struct
+
+    dim, n = 3, 4099
+    s_np = orc.random_state(dim, n, seed=31)
+    want = orc.flux(dim, s_np)
+    s = to_dev(s_np, cuda)
+    outs = [torch.empty(n, dtype=torch.float64, device=cuda) for _ in range(15)]
+    # the direct entry points reject an output that is an input plane ...
+    bad = list(outs)
+    bad[3] = s[1]
+    with pytest.raises(fvb.ArgumentError):
+        fvb.flux(s, dim, out=bad)
+    # ... and partially overlapping planes, before any launch
+    buf = torch.empty(2 * n, dtype=torch.float64, device=cuda)
+    bad = list(outs)
+    bad[0], bad[1] = buf[:n], buf[5:n + 5]
+    with pytest.raises(fvb.ArgumentError):
+        fvb.flux(s, dim, out=bad)
+    # one plane named by two outputs holds the later item (the reference's
+    # item order)
+    dup = list(outs)
+    dup[1] = dup[0]
+    fvb.flux(s, dim, out=dup)
+    assert same_bits(to_host([dup[0]])[0], want[1])
+    # structural-key kernels evaluate in place, as JitKernel::Fn may:
+    # pressure written over its own rhoE leaf equals the oracle bit for bit
+    vals = {"half": 0.5, "gm1": 0.4}
+    pat = dict(fvb.patterns())["pressure3_f64"]
+    k = fvb.lookup(re.sub(r"Cd#(\w+);", lambda m: "Cd%016x;" % struct.unpack(
+        "<Q", struct.pack("<d", vals[m.group(1)]))[0], pat))
+    assert k.n_outputs == 1
+    slots = [None] * k.n_inputs
+    for ci in range(k.n_inputs):
+        slots[k.in_slot[ci]] = s[ci]
+    args = N.ptr_array([s[4].data_ptr()] + [t.data_ptr() for t in slots])
+    N.check(k.fn(ctypes.byref(k), 0, n, args, torch.cuda.current_stream().cuda_stream))
+    assert same_bits(to_host([s[4]])[0], orc.cons2prim(dim, s_np)[dim])
+
+
 def test_cuda_graph_capture(cuda, orc):
     dim, n = 3, 100_000
     s = fvb.synth_state(dim, n, seed=9)
