@@ -8,7 +8,8 @@
 // emitted as CUDA source, compiled by NVRTC for sm_100a with --fmad=false
 // (the reference's -ffp-contract=off), and loaded with the runtime library
 // API.  It is cached per key for the process lifetime, like the JIT cache
-// (backend_jit.cpp:240-253, 314-335).
+// (backend_jit.cpp:240-253, 314-335), and the compiled image is also kept
+// on disk (FVB_CACHE_DIR, below) so a new process skips NVRTC.
 //
 // Semantics follow the reference's emit / emit_as (backend_jit.cpp:179-205):
 // every node computes in its own precision, operands are converted to it
@@ -22,6 +23,11 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cerrno>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -395,6 +401,7 @@ struct Nvrtc {
     decltype(&nvrtcGetCUBINSize) cubin_size = nullptr;
     decltype(&nvrtcGetCUBIN) cubin = nullptr;
     decltype(&nvrtcDestroyProgram) destroy = nullptr;
+    int major = 0, minor = 0;
 };
 
 const Nvrtc& nvrtc() {
@@ -422,6 +429,8 @@ const Nvrtc& nvrtc() {
         n.cubin = reinterpret_cast<decltype(n.cubin)>(dlsym(h, "nvrtcGetCUBIN"));
         n.destroy = reinterpret_cast<decltype(n.destroy)>(dlsym(h, "nvrtcDestroyProgram"));
         n.ok = n.create && n.compile && n.log_size && n.log && n.cubin_size && n.cubin && n.destroy;
+        if (auto ver = reinterpret_cast<decltype(&nvrtcVersion)>(dlsym(h, "nvrtcVersion")))
+            ver(&n.major, &n.minor);
         if (!n.ok) n.why = "libnvrtc lacks a required symbol";
         return n;
     }();
@@ -461,6 +470,107 @@ fvb_status compile(const std::string& src, std::vector<char>* image, bool* spill
     return FVB_OK;
 }
 
+// ---- the on-disk image cache -------------------------------------------------------
+//
+// One file per compiled source: <dir>/<hash>.cubin holding a header, the
+// exact source text and NVRTC version it was built from (checked on read, so
+// a hash collision or a changed emitter or toolkit only misses), the ptxas
+// spill verdict and the image.  <dir> is $FVB_CACHE_DIR, else
+// $XDG_CACHE_HOME/fvb, else $HOME/.cache/fvb; FVB_CACHE_DIR=off disables it.
+// Files are written to a temporary name and renamed, so concurrent processes
+// never read a partial image.  Any I/O failure only means a recompile.
+
+constexpr char kCacheMagic[8] = {'F', 'V', 'B', 'C', 'U', 'B', '1', '\0'};
+
+std::string cache_dir() {
+    const char* v = std::getenv("FVB_CACHE_DIR");
+    if (v) return std::strcmp(v, "off") == 0 || !*v ? std::string() : std::string(v);
+    if (const char* x = std::getenv("XDG_CACHE_HOME"); x && *x) return std::string(x) + "/fvb";
+    if (const char* h = std::getenv("HOME"); h && *h) return std::string(h) + "/.cache/fvb";
+    return std::string();
+}
+
+std::string cache_tag(const std::string& src) {
+    const Nvrtc& nv = nvrtc();
+    return "nvrtc " + std::to_string(nv.major) + "." + std::to_string(nv.minor) + "\n" + src;
+}
+
+std::string cache_path(const std::string& dir, const std::string& tag) {
+    char name[40];
+    std::snprintf(name, sizeof name, "/%016zx.cubin", std::hash<std::string>()(tag));
+    return dir + name;
+}
+
+bool read_all(const std::string& path, std::string* out) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) return false;
+    char buf[1 << 16];
+    size_t got;
+    out->clear();
+    while ((got = std::fread(buf, 1, sizeof buf, f)) > 0) out->append(buf, got);
+    const bool ok = !std::ferror(f);
+    std::fclose(f);
+    return ok;
+}
+
+bool cache_get(const std::string& src, std::vector<char>* image, bool* spilled) {
+    const std::string dir = cache_dir();
+    if (dir.empty()) return false;
+    const std::string tag = cache_tag(src);
+    std::string blob;
+    if (!read_all(cache_path(dir, tag), &blob)) return false;
+    // magic | u64 tag length | tag | u8 spilled | u64 image length | image
+    size_t at = 0;
+    auto take = [&](void* dst, size_t n) {
+        if (blob.size() - at < n) return false;
+        std::memcpy(dst, blob.data() + at, n);
+        at += n;
+        return true;
+    };
+    char magic[8];
+    uint64_t tlen = 0, ilen = 0;
+    uint8_t sp = 0;
+    if (!take(magic, 8) || std::memcmp(magic, kCacheMagic, 8) || !take(&tlen, 8) ||
+        tlen != tag.size() || blob.compare(at, tlen, tag) != 0)
+        return false;
+    at += tlen;
+    if (!take(&sp, 1) || !take(&ilen, 8) || ilen == 0 || blob.size() - at != ilen) return false;
+    image->assign(blob.data() + at, blob.data() + at + ilen);
+    *spilled = sp != 0;
+    return true;
+}
+
+void cache_put(const std::string& src, const std::vector<char>& image, bool spilled) {
+    const std::string dir = cache_dir();
+    if (dir.empty() || image.empty()) return;
+    // mkdir -p
+    for (size_t at = 1; at <= dir.size(); ++at)
+        if (at == dir.size() || dir[at] == '/') {
+            const std::string part = dir.substr(0, at);
+            if (::mkdir(part.c_str(), 0755) != 0 && errno != EEXIST) return;
+        }
+    const std::string tag = cache_tag(src);
+    const std::string path = cache_path(dir, tag);
+    const std::string tmp = path + ".tmp." + std::to_string(::getpid());
+    FILE* f = std::fopen(tmp.c_str(), "wb");
+    if (!f) return;
+    const uint64_t tlen = tag.size(), ilen = image.size();
+    const uint8_t sp = spilled ? 1 : 0;
+    bool ok = std::fwrite(kCacheMagic, 1, 8, f) == 8 && std::fwrite(&tlen, 8, 1, f) == 1 &&
+              std::fwrite(tag.data(), 1, tlen, f) == tlen && std::fwrite(&sp, 1, 1, f) == 1 &&
+              std::fwrite(&ilen, 8, 1, f) == 1 &&
+              std::fwrite(image.data(), 1, ilen, f) == ilen;
+    ok = std::fclose(f) == 0 && ok;
+    if (!ok || std::rename(tmp.c_str(), path.c_str()) != 0) std::remove(tmp.c_str());
+}
+
+fvb_status compile_cached(const std::string& src, std::vector<char>* image, bool* spilled) {
+    if (cache_get(src, image, spilled)) return FVB_OK;
+    if (fvb_status st = compile(src, image, spilled)) return st;
+    cache_put(src, *image, *spilled);
+    return FVB_OK;
+}
+
 // Emit and compile a key: 256-bit accesses and a 2-CTA/SM register cap
 // first; without the cap when the tree would spill under it; 128-bit
 // accesses when the NVRTC in use predates sm_100's 256-bit ones.
@@ -480,7 +590,7 @@ fvb_status build(const char* key, KDag* d, std::vector<char>* image, int* minb_o
                 return fail(FVB_EUNSUPPORTED, std::string("not a loweable structural key: ") +
                                                   std::string(key).substr(0, 160));
             bool spilled = false;
-            last = compile(src, image, &spilled);
+            last = compile_cached(src, image, &spilled);
             if (env_int("FVB_LOWER_DEBUG", 0))
                 std::fprintf(stderr, "[fvb lower] %016zx wide=%d minb=%d status=%d spilled=%d %s\n",
                              std::hash<std::string>()(key), int(wide), minb, int(last),

@@ -10,6 +10,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+# Every lowered kernel the tests use is compiled fresh: the on-disk image
+# cache points at a directory private to this session.
+if "FVB_CACHE_DIR" not in os.environ:
+    import tempfile
+    os.environ["FVB_CACHE_DIR"] = tempfile.mkdtemp(prefix="fvb-test-cache-")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs under gpurun / the driver)")

@@ -672,7 +672,7 @@ void run_gpu() {
         return "kernel " + name;
     });
 
-    check("errors: unsupported expression, length mismatch, shape mismatch", [&] {
+    check("errors: unsupported expression, length/shape mismatch, tag conflict, empty tree", [&] {
         DenseVector a(Precision::f64, 10), b(Precision::f64, 11), out(Precision::f64, 10);
         bool threw = false;
         try {  // a non-finite constant: the reference's JIT refuses such trees too
@@ -710,6 +710,22 @@ void run_gpu() {
             threw = true;
         }
         if (!threw) fail("no ShapeMismatch");
+        threw = false;
+        try {  // validate(): one tag bound to two different leaves (backend_eval.cpp:245-250)
+            DenseVector c(Precision::f64, 10);
+            dev::evaluate(be, tag(1, leaf(a)) + tag(1, leaf(c)), out);
+        } catch (const TagConflict&) {
+            threw = true;
+        }
+        if (!threw) fail("no TagConflict");
+        dev::evaluate(be, tag(1, leaf(a)) + tag(1, leaf(a)), out);  // same leaf: fine
+        threw = false;
+        try {
+            dev::evaluate(be, Expr(), out);
+        } catch (const Error&) {
+            threw = true;
+        }
+        if (!threw) fail("empty expression did not throw");
         return "";
     });
 }

@@ -6,6 +6,7 @@ import ctypes
 import os
 import re
 import subprocess
+import sys
 
 import pytest
 
@@ -205,3 +206,32 @@ def test_inconsistent_named_constant_rejected():
     except fvb.DeviceError:
         pass
     assert "(0x1p-1)" in fvb.emit_source(key)
+
+
+def _compile_in_subprocess(env_extra, key):
+    code = ("import sys, paper_1809_09851_b200 as fvb; "
+            "print(fvb.nvrtc_compile(sys.argv[1]))")
+    env = dict(os.environ, **env_extra)
+    out = subprocess.run([sys.executable, "-c", code, key], cwd=ROOT, env=env, check=True,
+                         capture_output=True, text=True).stdout
+    return int(out.strip())
+
+
+def test_lowered_images_are_cached_on_disk(tmp_path):
+    # A new process reuses the compiled image (FVB_CACHE_DIR); a damaged
+    # file is only a miss, and "off" writes nothing.
+    key = "dB4d(U11d(Ld0;),B7d(Ld1;,U20d(Ld0;)))"
+    d = tmp_path / "c"
+    size = _compile_in_subprocess({"FVB_CACHE_DIR": str(d)}, key)
+    files = sorted(d.glob("*.cubin"))
+    assert size > 0 and len(files) == 1
+    blob = files[0].read_bytes()
+    assert blob.startswith(b"FVBCUB1\0")
+    assert _compile_in_subprocess({"FVB_CACHE_DIR": str(d)}, key) == size
+    files[0].write_bytes(blob[: len(blob) // 2])  # truncated: recompiled and rewritten
+    assert _compile_in_subprocess({"FVB_CACHE_DIR": str(d)}, key) == size
+    assert files[0].read_bytes() == blob
+    off = tmp_path / "off"
+    assert _compile_in_subprocess({"FVB_CACHE_DIR": "off", "HOME": str(off),
+                                   "XDG_CACHE_HOME": ""}, key) == size
+    assert not off.exists()
