@@ -84,7 +84,9 @@ typedef enum fvb_status {
     FVB_ENCCL = 4,        /* collective failure (reserved for the host runtime)  */
     FVB_EARG = 5,         /* bad argument: NULL plane, dim out of range, ...     */
     FVB_EUNSUPPORTED = 6, /* no kernel for this structural key                   */
-    FVB_EALIGN = 7        /* a plane pointer is not element-aligned              */
+    FVB_EALIGN = 7,       /* a plane pointer is not element-aligned              */
+    FVB_EHOST = 8         /* host-side failure: memory, threads (no exception    */
+                          /* ever crosses this ABI)                              */
 } fvb_status;
 
 typedef enum fvb_prec { FVB_F32 = 0, FVB_F64 = 1 } fvb_prec;

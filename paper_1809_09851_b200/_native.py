@@ -51,6 +51,7 @@ FVB_ENCCL = 4
 FVB_EARG = 5
 FVB_EUNSUPPORTED = 6
 FVB_EALIGN = 7
+FVB_EHOST = 8
 
 
 class FvbError(RuntimeError):
@@ -89,6 +90,7 @@ _ERRORS = {
     FVB_EARG: ArgumentError,
     FVB_EUNSUPPORTED: UnsupportedExpression,
     FVB_EALIGN: ArgumentError,
+    FVB_EHOST: FvbError,
 }
 
 

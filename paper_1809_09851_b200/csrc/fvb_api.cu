@@ -21,12 +21,18 @@ thread_local std::string t_error;
 }
 
 fvb_status fail(fvb_status s, const std::string& msg) {
-    t_error = msg;
+    try {
+        t_error = msg;
+    } catch (...) {  // keep the status; the message is best effort
+    }
     return s;
 }
 
 fvb_status cuda_fail(cudaError_t e, const char* what) {
-    t_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    try {
+        t_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    } catch (...) {
+    }
     return FVB_ECUDA;
 }
 

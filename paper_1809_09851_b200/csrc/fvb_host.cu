@@ -84,17 +84,24 @@ struct PassThrough {
         const unsigned nt = std::min(8u, std::max(1u, hw / 2));
         const size_t total = size_t(pass) * bytes;
         const size_t per = (total + nt - 1) / nt;
-        for (unsigned t = 0; t < nt; ++t) {
-            workers.emplace_back([=] {
-                size_t lo = size_t(t) * per, hi = std::min(total, lo + per);
-                while (lo < hi) {
-                    const size_t plane = lo / bytes, at = lo % bytes;
-                    const size_t len = std::min(hi - lo, bytes - at);
-                    std::memcpy(static_cast<char*>(out[plane]) + at,
-                                static_cast<const char*>(in[1 + plane]) + at, len);
-                    lo += len;
-                }
-            });
+        auto copy = [=](size_t lo, size_t hi) {
+            while (lo < hi) {
+                const size_t plane = lo / bytes, at = lo % bytes;
+                const size_t len = std::min(hi - lo, bytes - at);
+                std::memcpy(static_cast<char*>(out[plane]) + at,
+                            static_cast<const char*>(in[1 + plane]) + at, len);
+                lo += len;
+            }
+        };
+        try {
+            for (unsigned t = 0; t < nt; ++t) {
+                const size_t lo = size_t(t) * per;
+                workers.emplace_back(copy, lo, std::min(total, lo + per));
+            }
+        } catch (...) {  // no threads to be had: copy on the calling thread
+            for (auto& w : workers) w.join();
+            workers.clear();
+            copy(0, total);
         }
     }
     ~PassThrough() {
@@ -219,7 +226,7 @@ fvb_status fvb_ctx_create(int device, uint64_t chunk_points, fvb_ctx** out) {
     if (e != cudaSuccess) return cuda_fail(e, "device query");
     if (device < 0 || device >= count) return fail(FVB_EARG, "device ordinal out of range");
     auto* ctx = new (std::nothrow) fvb_ctx;
-    if (!ctx) return fail(FVB_EARG, "out of host memory");
+    if (!ctx) return fail(FVB_EHOST, "out of host memory");
     ctx->device = device;
     ctx->chunk_points = chunk_points;
     DeviceGuard guard(device);
@@ -251,24 +258,28 @@ fvb_status fvb_ctx_destroy(fvb_ctx* ctx) {
 
 fvb_status fvb_flux_host(fvb_ctx* ctx, const fvb_gas* gas, uint32_t dim, uint8_t prec,
                          uint64_t n, const void* const* in, void* const* out) {
-    if (fvb_status st = check(ctx, gas, dim, prec)) return st;
-    if (prec == FVB_F64)
-        return pipeline_dim<FluxOp, false, double, true, true>(ctx, gas, dim, in, out, n, nullptr);
-    return pipeline_dim<FluxOp, false, float, true, true>(ctx, gas, dim, in, out, n, nullptr);
+    return guarded([&]() -> fvb_status {
+        if (fvb_status st = check(ctx, gas, dim, prec)) return st;
+        if (prec == FVB_F64)
+            return pipeline_dim<FluxOp, false, double, true, true>(ctx, gas, dim, in, out, n, nullptr);
+        return pipeline_dim<FluxOp, false, float, true, true>(ctx, gas, dim, in, out, n, nullptr);
+    });
 }
 
 fvb_status fvb_jacobian_host(fvb_ctx* ctx, const fvb_gas* gas, uint32_t dim, uint8_t prec,
                              uint64_t n, const void* const* in, void* const* out,
                              double* lambda_max) {
-    if (fvb_status st = check(ctx, gas, dim, prec)) return st;
-    if (prec == FVB_F64) {
+    return guarded([&]() -> fvb_status {
+        if (fvb_status st = check(ctx, gas, dim, prec)) return st;
+        if (prec == FVB_F64) {
+            if (lambda_max)
+                return pipeline_dim<JacobianOp, true, double>(ctx, gas, dim, in, out, n, lambda_max);
+            return pipeline_dim<JacobianOp, false, double>(ctx, gas, dim, in, out, n, nullptr);
+        }
         if (lambda_max)
-            return pipeline_dim<JacobianOp, true, double>(ctx, gas, dim, in, out, n, lambda_max);
-        return pipeline_dim<JacobianOp, false, double>(ctx, gas, dim, in, out, n, nullptr);
-    }
-    if (lambda_max)
-        return pipeline_dim<JacobianOp, true, float>(ctx, gas, dim, in, out, n, lambda_max);
-    return pipeline_dim<JacobianOp, false, float>(ctx, gas, dim, in, out, n, nullptr);
+            return pipeline_dim<JacobianOp, true, float>(ctx, gas, dim, in, out, n, lambda_max);
+        return pipeline_dim<JacobianOp, false, float>(ctx, gas, dim, in, out, n, nullptr);
+    });
 }
 
 }  // extern "C"

@@ -11,6 +11,8 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <exception>
+#include <new>
 #include <string>
 
 #include "fvb.h"
@@ -23,6 +25,21 @@ fvb_status fail(fvb_status s, const std::string& msg);
 fvb_status cuda_fail(cudaError_t e, const char* what);
 
 int device_sm_count();
+
+// No C++ exception crosses the C ABI: entry points whose host side
+// allocates (keys, NVRTC, host threads) run their body under this guard.
+template <class F>
+fvb_status guarded(F&& body) noexcept {
+    try {
+        return body();
+    } catch (const std::bad_alloc&) {
+        return fail(FVB_EHOST, "host memory exhausted");
+    } catch (const std::exception& e) {
+        return fail(FVB_EHOST, e.what());
+    } catch (...) {
+        return fail(FVB_EHOST, "unexpected host-side exception");
+    }
+}
 
 // Launch tuning, read once from the environment (bench sweeps only; the
 // defaults are the measured best):

@@ -707,27 +707,31 @@ using namespace fvb;
 extern "C" {
 
 fvb_status fvb_emit_source(const char* key, char* buf, size_t cap, size_t* len) {
-    if (!key) return fail(FVB_EARG, "NULL key");
-    std::string src;
-    if (!emit(key, &src, nullptr))
-        return fail(FVB_EUNSUPPORTED, "not a loweable structural key");
-    if (len) *len = src.size();
-    if (buf && cap) {
-        const size_t n = src.size() < cap - 1 ? src.size() : cap - 1;
-        std::memcpy(buf, src.data(), n);
-        buf[n] = '\0';
-    }
-    return FVB_OK;
+    return guarded([&]() -> fvb_status {
+        if (!key) return fail(FVB_EARG, "NULL key");
+        std::string src;
+        if (!emit(key, &src, nullptr))
+            return fail(FVB_EUNSUPPORTED, "not a loweable structural key");
+        if (len) *len = src.size();
+        if (buf && cap) {
+            const size_t n = src.size() < cap - 1 ? src.size() : cap - 1;
+            std::memcpy(buf, src.data(), n);
+            buf[n] = '\0';
+        }
+        return FVB_OK;
+    });
 }
 
 fvb_status fvb_nvrtc_compile(const char* key, size_t* cubin_bytes) {
-    if (!key) return fail(FVB_EARG, "NULL key");
-    KDag d;
-    std::vector<char> image;
-    int minb = 2;
-    if (fvb_status st = build(key, &d, &image, &minb)) return st;
-    if (cubin_bytes) *cubin_bytes = image.size();
-    return FVB_OK;
+    return guarded([&]() -> fvb_status {
+        if (!key) return fail(FVB_EARG, "NULL key");
+        KDag d;
+        std::vector<char> image;
+        int minb = 2;
+        if (fvb_status st = build(key, &d, &image, &minb)) return st;
+        if (cubin_bytes) *cubin_bytes = image.size();
+        return FVB_OK;
+    });
 }
 
 }  // extern "C"

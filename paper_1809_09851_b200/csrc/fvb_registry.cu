@@ -505,53 +505,65 @@ using namespace fvb;
 extern "C" {
 
 fvb_status fvb_lookup(const char* key, fvb_kernel* out) {
-    if (!key || !out) return fail(FVB_EARG, "NULL key or output");
-    // FVB_FORCE_LOWER=1 skips the hand-written kernels (tests and the
-    // hand-written-vs-lowered comparison run the same trees both ways).
-    static const bool force_lower = [] {
-        const char* v = std::getenv("FVB_FORCE_LOWER");
-        return v && *v && *v != '0';
-    }();
-    if (force_lower) return lower_lookup(key, out);
-    for (const Pattern& p : patterns()) {
-        double consts[8] = {0};
-        bool seen[8] = {false};
-        if (!match(p.text, key, consts, seen)) continue;
-        fvb_kernel k;
-        std::memset(&k, 0, sizeof k);
-        k.fn = p.fn;
-        k.reduce = p.reduce;
-        k.n_outputs = p.n_outputs;
-        k.n_inputs = uint32_t(p.slots.size());
-        k.n_consts = kNumConsts;
-        k.prec = p.prec;
-        k.dim = p.dim;
-        // Constants the key did not carry (e.g. the Jacobian's 0 and 1 in a
-        // block without them) keep the default gas values, narrowed.
-        const fvb_gas dflt{2.0 / 5.0, 7.0 / 5.0, 5.0 / 2.0};
-        const double defaults[kNumConsts] = {0.5, dflt.gamma_minus_one, dflt.gamma, dflt.cv, 0.0,
-                                             1.0};
-        for (int c = 0; c < kNumConsts; ++c)
-            k.consts[c] = seen[c] ? consts[c]
-                                  : (p.prec ? defaults[c] : double(float(defaults[c])));
-        for (int i = 0; i < 8; ++i) k.in_slot[i] = -1;
-        for (size_t i = 0; i < p.canon.size() && i < 8; ++i)
-            for (size_t s = 0; s < p.slots.size(); ++s)
-                if (p.slots[s] == p.canon[i]) k.in_slot[i] = int8_t(s);
-        std::snprintf(k.name, sizeof k.name, "%s", p.name.c_str());
-        *out = k;
-        return FVB_OK;
-    }
-    // No hand-written kernel: lower the tree itself (NVRTC, cached per key).
-    return lower_lookup(key, out);
+    return guarded([&]() -> fvb_status {
+        if (!key || !out) return fail(FVB_EARG, "NULL key or output");
+        // FVB_FORCE_LOWER=1 skips the hand-written kernels (tests and the
+        // hand-written-vs-lowered comparison run the same trees both ways).
+        static const bool force_lower = [] {
+            const char* v = std::getenv("FVB_FORCE_LOWER");
+            return v && *v && *v != '0';
+        }();
+        if (force_lower) return lower_lookup(key, out);
+        for (const Pattern& p : patterns()) {
+            double consts[8] = {0};
+            bool seen[8] = {false};
+            if (!match(p.text, key, consts, seen)) continue;
+            fvb_kernel k;
+            std::memset(&k, 0, sizeof k);
+            k.fn = p.fn;
+            k.reduce = p.reduce;
+            k.n_outputs = p.n_outputs;
+            k.n_inputs = uint32_t(p.slots.size());
+            k.n_consts = kNumConsts;
+            k.prec = p.prec;
+            k.dim = p.dim;
+            // Constants the key did not carry (e.g. the Jacobian's 0 and 1 in a
+            // block without them) keep the default gas values, narrowed.
+            const fvb_gas dflt{2.0 / 5.0, 7.0 / 5.0, 5.0 / 2.0};
+            const double defaults[kNumConsts] = {0.5, dflt.gamma_minus_one, dflt.gamma, dflt.cv, 0.0,
+                                                 1.0};
+            for (int c = 0; c < kNumConsts; ++c)
+                k.consts[c] = seen[c] ? consts[c]
+                                      : (p.prec ? defaults[c] : double(float(defaults[c])));
+            for (int i = 0; i < 8; ++i) k.in_slot[i] = -1;
+            for (size_t i = 0; i < p.canon.size() && i < 8; ++i)
+                for (size_t s = 0; s < p.slots.size(); ++s)
+                    if (p.slots[s] == p.canon[i]) k.in_slot[i] = int8_t(s);
+            std::snprintf(k.name, sizeof k.name, "%s", p.name.c_str());
+            *out = k;
+            return FVB_OK;
+        }
+        // No hand-written kernel: lower the tree itself (NVRTC, cached per key).
+        return lower_lookup(key, out);
+    });
 }
 
-uint32_t fvb_pattern_count(void) { return uint32_t(patterns().size()); }
+uint32_t fvb_pattern_count(void) {
+    try {
+        return uint32_t(patterns().size());
+    } catch (...) {
+        return 0;
+    }
+}
 
 const char* fvb_pattern(uint32_t i, const char** name) {
-    if (i >= patterns().size()) return nullptr;
-    if (name) *name = patterns()[i].name.c_str();
-    return patterns()[i].text.c_str();
+    try {
+        if (i >= patterns().size()) return nullptr;
+        if (name) *name = patterns()[i].name.c_str();
+        return patterns()[i].text.c_str();
+    } catch (...) {
+        return nullptr;
+    }
 }
 
 }  // extern "C"

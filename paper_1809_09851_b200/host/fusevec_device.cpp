@@ -384,7 +384,11 @@ bool try_plan(const std::vector<Expr>& items, std::vector<Out> outs, std::size_t
         if (key.empty()) return false;
     }
     fvb_kernel k;
-    if (fvb_lookup(key.c_str(), &k) != FVB_OK) return false;
+    // Only "no kernel for this key" is a miss; a device or host failure while
+    // lowering (NVRTC, module load) surfaces as its own exception.
+    const fvb_status st = fvb_lookup(key.c_str(), &k);
+    if (st == FVB_EUNSUPPORTED) return false;
+    fvb_check(st);
     if (k.n_outputs != outs.size() || k.n_inputs != leaves.size()) return false;
     plan->k = k;
     plan->leaves = std::move(leaves);
