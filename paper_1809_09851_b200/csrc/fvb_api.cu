@@ -6,6 +6,7 @@
 // validate() throws before evaluating: proj/src/backend_eval.cpp:236-265).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -37,16 +38,16 @@ fvb_status cuda_fail(cudaError_t e, const char* what) {
 }
 
 int device_sm_count() {
-    static int counts[64] = {0};
+    static std::atomic<int> counts[64];  // 0 = not queried yet
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
-    if (!counts[dev]) {
-        int c = 0;
+    int c = counts[dev].load(std::memory_order_relaxed);
+    if (!c) {
         if (cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || c < 1)
             c = 148;
-        counts[dev] = c;
+        counts[dev].store(c, std::memory_order_relaxed);
     }
-    return counts[dev];
+    return c;
 }
 
 const Tuning& tuning() {
