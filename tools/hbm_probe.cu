@@ -74,6 +74,14 @@ __device__ __forceinline__ void body(const P<R, W>& p, unsigned long long g0,
 #pragma unroll
                     for (int q = 0; q < V; ++q) acc = acc + x[u][i][q];
             }
+            if constexpr (W > 0 && W < R) {
+                // fewer outputs than inputs: every input must feed a store,
+                // or ptxas drops the unused loads (the mix would be a lie)
+#pragma unroll
+                for (int i = 1; i < R; ++i)
+#pragma unroll
+                    for (int q = 0; q < V; ++q) x[u][0][q] = x[u][0][q] + x[u][i][q];
+            }
 #pragma unroll
             for (int j = 0; j < W; ++j) stv<V>(p.out[j] + g * V, x[u][j % R]);
         }
@@ -105,6 +113,12 @@ __global__ void __launch_bounds__(256) stream_kernel(P<R, W> p, unsigned long lo
             double x[R][V];
 #pragma unroll
             for (int i = 0; i < R; ++i) ldv<V>(p.in[i] + g * V, x[i]);
+            if constexpr (W < R) {
+#pragma unroll
+                for (int i = 1; i < R; ++i)
+#pragma unroll
+                    for (int q = 0; q < V; ++q) x[0][q] = x[0][q] + x[i][q];
+            }
 #pragma unroll
             for (int j = 0; j < W; ++j) {
                 const int slot = j & 3;
