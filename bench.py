@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--impl", default="fvb", choices=["fvb", "reference"])
     ap.add_argument("--config", default="flux3d", choices=sorted(CONFIGS))
     ap.add_argument("--prec", default="f64", choices=["f64", "f32"])
-    ap.add_argument("--n", type=int, default=0, help="points per GPU (default: the config's)")
+    ap.add_argument("--n", "--points", dest="n", type=int, default=0,
+                    help="points per GPU (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-points", type=int, default=0,
                     help="points per rank for e2e (0: all at N=1, 2.5e7 at N>1)")
@@ -426,6 +427,22 @@ def device_run(a, rank, world, local):
 def main():
     a = parse()
     rank, world, local = dist_env()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched directly with --gpus N: re-launch as N ranks, one per GPU,
+        # exactly as the driver does
+        import socket
+        with socket.socket() as sock:
+            sock.bind(("127.0.0.1", 0))
+            port = sock.getsockname()[1]
+        # (--n is spelled --points: torchrun's parser would take "--n" as an
+        # ambiguous prefix of its own options)
+        args = ["--points" + x[3:] if x == "--n" or x.startswith("--n=") else x
+                for x in sys.argv[1:]]
+        os.execv(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                  f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1",
+                                  "--master-port", str(port), os.path.abspath(__file__)] + args)
+    if "WORLD_SIZE" in os.environ and a.gpus != world:
+        print(f"bench: --gpus {a.gpus} but WORLD_SIZE={world}; using {world}", file=sys.stderr)
     # stdout carries exactly one JSON line: everything else any library
     # prints to fd 1 (e.g. NCCL's version banner at init) goes to stderr.
     sys.stdout.flush()
