@@ -28,13 +28,32 @@ def weak_slice(rank: int, n_per_rank: int):
     return rank * n_per_rank, (rank + 1) * n_per_rank
 
 
+_SIGN = {8: -0x8000000000000000, 4: -0x80000000}
+
+
 def allreduce_max(t, group=None):
-    """In-place all-reduce(MAX) of a 0-d/1-element tensor over the process
-    group; a no-op without an initialised group (single process)."""
+    """In-place all-reduce(MAX) of a 0-d/1-element float tensor over the
+    process group; a no-op without an initialised group (single process).
+
+    The maximum is taken over the IEEE bit patterns as unsigned integers,
+    exactly like the device reduction (fvb_stream.cuh: atomicMax on the
+    bits): wave speeds are >= 0, where that order is the numeric order, and
+    a NaN on any rank wins on every rank instead of depending on the
+    backend's float max.  The unsigned order is carried in a signed
+    all-reduce by flipping the sign bit."""
+    import torch
     import torch.distributed as dist
 
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    if not (dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1):
+        return t
+    ity = {torch.float64: torch.int64, torch.float32: torch.int32}.get(t.dtype)
+    if ity is None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        return t
+    flip = _SIGN[t.element_size()]
+    key = t.view(ity) ^ flip
+    dist.all_reduce(key, op=dist.ReduceOp.MAX, group=group)
+    t.view(ity).copy_(key ^ flip)
     return t
 
 

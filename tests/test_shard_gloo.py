@@ -73,3 +73,37 @@ def test_cfl_allreduce_max_gloo_world2(orc, n_total):
     assert [result[r] for r in range(world)] == [whole] * world
     # and bitwise: the global max is one of the per-point values
     assert np.float64(whole).tobytes() == np.float64(result[0]).tobytes()
+
+
+def _nan_worker(rank, world, port, values, result):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = []
+    for case in values:
+        for dt in (torch.float64, torch.float32):
+            t = torch.tensor([case[rank]], dtype=dt)
+            shard.allreduce_max(t)
+            out.append(t.view(torch.int64 if dt == torch.float64 else torch.int32).item())
+    result[rank] = out
+    dist.destroy_process_group()
+
+
+def test_cfl_allreduce_is_the_unsigned_bit_max(orc):
+    # the cross-rank max follows the device reduction: IEEE bits compared as
+    # unsigned integers, so a NaN on any rank reaches every rank, inf beats
+    # every finite speed, and +0 < every positive speed
+    nan, inf = float("nan"), float("inf")
+    cases = [(1.5, 2.5), (2.5, 1.5), (nan, 3.0), (3.0, nan), (inf, 7.0), (0.0, 1e-300),
+             (0.0, 0.0), (-nan, 1.0)]
+    world = 2
+    mgr = mp.Manager()
+    result = mgr.dict()
+    mp.spawn(_nan_worker, args=(world, _free_port(), cases, result), nprocs=world, join=True)
+    want = []
+    for case in cases:
+        for np_t, ui in ((np.float64, np.uint64), (np.float32, np.uint32)):
+            bits = [int(np.array([v], np_t).view(ui)[0]) for v in case]
+            b = max(bits)
+            want.append(int(np.array([b], ui).view(np.int64 if ui == np.uint64 else np.int32)[0]))
+    assert result[0] == result[1] == want
