@@ -258,7 +258,8 @@ FVB_API const char* fvb_pattern(uint32_t i, const char** name);
 
 /* A per-device context owning staging buffers and copy/compute streams for
  * the host-buffer entry points.  chunk_points = points per pipeline stage
- * (0 = default 4 Mi). */
+ * (0 = as many as fit 256 MiB of device staging per slot).  Not thread-safe:
+ * one call at a time per context. */
 typedef struct fvb_ctx fvb_ctx;
 FVB_API fvb_status fvb_ctx_create(int device, uint64_t chunk_points, fvb_ctx** out);
 FVB_API fvb_status fvb_ctx_destroy(fvb_ctx* ctx);
@@ -273,6 +274,25 @@ FVB_API fvb_status fvb_flux_host(fvb_ctx* ctx, const fvb_gas* gas, uint32_t dim,
 FVB_API fvb_status fvb_jacobian_host(fvb_ctx* ctx, const fvb_gas* gas, uint32_t dim, uint8_t prec,
                              uint64_t n, const void* const* in, void* const* out,
                              double* lambda_max);
+
+/* Any structural-key kernel (fvb_lookup) over HOST arrays: the staged
+ * executor behind the two calls above, for the C++ adapter's host
+ * DenseVectors.  args is the kernel's argument block (k->n_outputs outputs,
+ * then k->n_inputs leaves in slot order); arg_prec[i] is 0 (f32) or 1 (f64);
+ * arg_on_device[i] = 1 marks a DEVICE plane used in place, 2 an output the
+ * caller does not want back (computed into device scratch only, e.g. a
+ * pass-through item the caller copies host-side); NULL = all host.
+ * Host planes may be pinned or pageable: pageable ones are packed into
+ * pinned bounce buffers by host threads, overlapped with the device work.
+ * An output may be one of the host leaves (in-place evaluation); a NULL
+ * output slot is allowed where the kernel allows it.  With lambda_max
+ * (HOST double) the kernel's CFL reduction runs as well.  Device work
+ * already queued on `after` (a cudaStream_t, may be NULL) completes before
+ * the call reads any plane.  Returns once every output is in place. */
+FVB_API fvb_status fvb_launch_host(fvb_ctx* ctx, const fvb_kernel* k, uint64_t n,
+                                   void* const* args, const uint8_t* arg_prec,
+                                   const uint8_t* arg_on_device, double* lambda_max,
+                                   void* after);
 
 #ifdef __cplusplus
 }

@@ -41,6 +41,7 @@ EXPORTED = (
     "fvb_ctx_destroy",
     "fvb_flux_host",
     "fvb_jacobian_host",
+    "fvb_launch_host",
 )
 
 FVB_OK = 0
@@ -166,6 +167,8 @@ def _declare(L):
         "fvb_flux_host": (i32, [vp, gas, u32, u8, u64, pp, pp]),
         "fvb_jacobian_host": (i32, [vp, gas, u32, u8, u64, pp, pp,
                                     ctypes.POINTER(ctypes.c_double)]),
+        "fvb_launch_host": (i32, [vp, ctypes.POINTER(KernelStruct), u64, pp, vp, vp,
+                                  ctypes.POINTER(ctypes.c_double), vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -1,18 +1,29 @@
-// fvb_host.cu -- the host-buffer (end-to-end) path: fvb_ctx and the
-// streamed fvb_flux_host / fvb_jacobian_host.
+// fvb_host.cu -- the host-buffer (end-to-end) path: fvb_ctx, the staged
+// executor behind it, and fvb_flux_host / fvb_jacobian_host /
+// fvb_launch_host.
 //
 // The reference evaluates host DenseVectors in place (proj/src/
 // backend_eval.cpp:280-346).  A drop-in device backend handed host buffers
-// must move them over PCIe; this path hides the kernel entirely behind the
-// copies: the range is cut into chunks, and chunk c runs on slot c % kSlots
-// as [H2D inputs -> fused kernel -> D2H outputs] in that slot's stream, so
-// the H2D of one chunk, the kernel of another and the D2H of a third overlap
-// on the two copy directions.  Slot buffers are reused in stream order; the
-// host synchronises once, at the end.
+// must move them over PCIe; this path hides the kernel behind the copies.
+// The range is cut into chunks, and chunk c runs on slot c % kSlots as
+// [H2D inputs -> fused kernel -> D2H outputs] in that slot's stream, so the
+// H2D of one chunk, the kernel of another and the D2H of a third overlap on
+// the two copy directions.
+//
+// Host planes may be pinned or pageable (the reference's DenseVectors are
+// ordinary heap memory).  Pinned planes are DMA'd directly.  Pageable ones
+// go through pinned bounce buffers of the slot: a pool of host threads packs
+// chunk c's pageable inputs while the device still works on chunks c-1 and
+// c-2, and unpacks a chunk's outputs once its D2H has completed.  Device
+// planes (resident leaves, device destinations) are used in place.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <new>
 #include <thread>
 #include <vector>
@@ -20,15 +31,104 @@
 #include "fvb.h"
 #include "fvb_launch.cuh"
 
+namespace fvb {
+namespace {
+
+// ---- a small pool of copy threads -------------------------------------------------
+
+struct Piece {
+    char* dst;
+    const char* src;
+    size_t bytes;
+};
+
+class CopyPool {
+  public:
+    explicit CopyPool(unsigned workers) {
+        try {
+            for (unsigned t = 0; t < workers; ++t) threads_.emplace_back([this] { loop(); });
+        } catch (...) {  // fewer threads than asked: the caller still copies
+            stop_workers();
+        }
+    }
+    ~CopyPool() { stop_workers(); }
+
+    // Every piece copied when this returns; the calling thread helps.
+    void run(const std::vector<Piece>& pieces) {
+        if (pieces.empty()) return;
+        if (threads_.empty() || pieces.size() == 1) {
+            for (const Piece& p : pieces) std::memcpy(p.dst, p.src, p.bytes);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            work_ = &pieces;
+            next_.store(0);
+            pending_ = unsigned(threads_.size());
+            ++gen_;
+        }
+        cv_.notify_all();
+        drain(pieces);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [this] { return pending_ == 0; });
+        work_ = nullptr;
+    }
+
+  private:
+    void drain(const std::vector<Piece>& pieces) {
+        for (size_t i; (i = next_.fetch_add(1)) < pieces.size();)
+            std::memcpy(pieces[i].dst, pieces[i].src, pieces[i].bytes);
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+            const std::vector<Piece>* w = work_;
+            lk.unlock();
+            drain(*w);
+            lk.lock();
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    void stop_workers() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : threads_) t.join();
+        threads_.clear();
+    }
+
+    std::mutex mu_;
+    std::condition_variable cv_, done_;
+    std::vector<std::thread> threads_;
+    const std::vector<Piece>* work_ = nullptr;
+    std::atomic<size_t> next_{0};
+    unsigned pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+}  // namespace
+}  // namespace fvb
+
 struct fvb_ctx {
     static constexpr int kSlots = 3;
     int device = 0;
     uint64_t chunk_points = 0;  // 0 = size chunks by bytes
     cudaStream_t stream[kSlots] = {};
-    void* slot_buf[kSlots] = {};
+    cudaEvent_t done[kSlots] = {};  // the slot's last D2H has completed
+    void* slot_buf[kSlots] = {};    // device staging
     size_t slot_bytes = 0;
-    void* red = nullptr;  // lambda-max accumulator (8 bytes)
+    void* pin_buf[kSlots] = {};     // pinned bounce buffers for pageable planes
+    size_t pin_bytes = 0;
+    void* red = nullptr;            // lambda-max accumulator (8 bytes)
     cudaEvent_t reset_done = nullptr;
+    std::unique_ptr<fvb::CopyPool> pool;
 };
 
 namespace fvb {
@@ -45,30 +145,217 @@ struct DeviceGuard {
     }
 };
 
-fvb_status ensure_slots(fvb_ctx* ctx, size_t bytes) {
-    if (bytes <= ctx->slot_bytes) return FVB_OK;
-    for (int s = 0; s < fvb_ctx::kSlots; ++s) {
-        if (ctx->slot_buf[s]) {
-            cudaStreamSynchronize(ctx->stream[s]);
-            cudaFree(ctx->slot_buf[s]);
+fvb_status ensure_buffers(fvb_ctx* ctx, size_t dev_bytes, size_t pin_bytes) {
+    if (dev_bytes > ctx->slot_bytes || pin_bytes > ctx->pin_bytes) {
+        for (int s = 0; s < fvb_ctx::kSlots; ++s) cudaStreamSynchronize(ctx->stream[s]);
+    }
+    if (dev_bytes > ctx->slot_bytes) {
+        for (int s = 0; s < fvb_ctx::kSlots; ++s) {
+            if (ctx->slot_buf[s]) cudaFree(ctx->slot_buf[s]);
             ctx->slot_buf[s] = nullptr;
         }
+        ctx->slot_bytes = 0;
+        for (int s = 0; s < fvb_ctx::kSlots; ++s) {
+            const cudaError_t e = cudaMalloc(&ctx->slot_buf[s], dev_bytes);
+            if (e != cudaSuccess) return cuda_fail(e, "staging allocation");
+        }
+        ctx->slot_bytes = dev_bytes;
     }
-    ctx->slot_bytes = 0;
-    for (int s = 0; s < fvb_ctx::kSlots; ++s) {
-        const cudaError_t e = cudaMalloc(&ctx->slot_buf[s], bytes);
-        if (e != cudaSuccess) return cuda_fail(e, "staging allocation");
+    if (pin_bytes > ctx->pin_bytes) {
+        for (int s = 0; s < fvb_ctx::kSlots; ++s) {
+            if (ctx->pin_buf[s]) cudaFreeHost(ctx->pin_buf[s]);
+            ctx->pin_buf[s] = nullptr;
+        }
+        ctx->pin_bytes = 0;
+        for (int s = 0; s < fvb_ctx::kSlots; ++s) {
+            const cudaError_t e = cudaHostAlloc(&ctx->pin_buf[s], pin_bytes, cudaHostAllocDefault);
+            if (e != cudaSuccess) return cuda_fail(e, "pinned bounce allocation");
+        }
+        ctx->pin_bytes = pin_bytes;
     }
-    ctx->slot_bytes = bytes;
     return FVB_OK;
 }
 
-// Chunk size: 256 MiB of planes per slot unless the context fixes it.
+// Chunk size: 256 MiB of device staging per slot unless the context fixes it.
 uint64_t chunk_for(const fvb_ctx* ctx, size_t bytes_per_point, uint64_t n) {
     uint64_t c = ctx->chunk_points;
-    if (!c) c = (uint64_t(256) << 20) / bytes_per_point;
+    if (!c) c = (uint64_t(256) << 20) / std::max<size_t>(bytes_per_point, 1);
     c = std::max<uint64_t>(c & ~uint64_t(255), 256);  // keep 32-byte alignment of slot planes
     return std::min<uint64_t>(c, std::max<uint64_t>(n, 1));
+}
+
+enum class Mem { kPageable, kPinned, kDevice };
+
+Mem memory_kind(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();  // clear: unknown memory is pageable
+        return Mem::kPageable;
+    }
+    switch (a.type) {
+        case cudaMemoryTypeHost:
+        case cudaMemoryTypeManaged: return Mem::kPinned;
+        case cudaMemoryTypeDevice: return Mem::kDevice;
+        default: return Mem::kPageable;
+    }
+}
+
+// One plane of a staged launch.
+struct Arg {
+    char* host = nullptr;  // host plane (pinned or pageable), or
+    char* dev = nullptr;   // a device plane used in place; both NULL = NULL slot
+    size_t width = 8;
+    bool out = false;
+    int alias = -1;        // output: index of the host input whose staging it shares
+    bool scratch = false;  // output with a device slot only (written, never copied back)
+    // assigned by staged():
+    bool pinned = false;
+    size_t dev_off = 0, pin_off = 0;  // byte offsets of the plane in a slot, per chunk element
+    bool has_pin = false;
+};
+
+// Pieces of at most 8 MiB, so the pool's threads share one plane's copy.
+void add_pieces(std::vector<Piece>& v, char* dst, const char* src, size_t bytes) {
+    constexpr size_t kPiece = size_t(8) << 20;
+    for (size_t at = 0; at < bytes; at += kPiece)
+        v.push_back({dst + at, src + at, std::min(kPiece, bytes - at)});
+}
+
+// The staged executor.  `launch(dev_args, cnt, stream)` enqueues the kernel
+// for one chunk; dev_args follow `args` (device pointers at the chunk, NULL
+// for NULL slots).  Returns once every output is in place.
+template <class Launch>
+fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& launch) {
+    // staging layout: inputs first, then outputs not sharing an input's slot
+    size_t dev_bpp = 0, pin_bpp = 0;
+    bool any_pageable = false;
+    for (Arg& a : args) {
+        if (a.scratch) {
+            a.dev_off = dev_bpp;
+            dev_bpp += a.width;
+            continue;
+        }
+        if (!a.host) continue;
+        const Mem kind = memory_kind(a.host);
+        if (kind == Mem::kDevice) return fail(FVB_EARG, "a host plane is device memory");
+        a.pinned = kind == Mem::kPinned;
+        if (a.out && a.alias >= 0) continue;
+        a.dev_off = dev_bpp;
+        dev_bpp += a.width;
+        if (!a.pinned) {
+            a.has_pin = true;
+            a.pin_off = pin_bpp;
+            pin_bpp += a.width;
+            any_pageable = true;
+        }
+    }
+    for (Arg& a : args)
+        if (a.host && a.out && a.alias >= 0) {
+            const Arg& src = args[size_t(a.alias)];
+            a.dev_off = src.dev_off;
+            a.pin_off = src.pin_off;
+            a.has_pin = !a.pinned;
+            if (a.has_pin && !src.has_pin) {  // pageable output over a pinned input: own bounce
+                a.pin_off = pin_bpp;
+                pin_bpp += a.width;
+                any_pageable = true;
+            }
+        }
+    const uint64_t chunk = chunk_for(ctx, std::max<size_t>(dev_bpp, 1), n);
+    if (fvb_status st = ensure_buffers(ctx, size_t(chunk) * dev_bpp, size_t(chunk) * pin_bpp))
+        return st;
+    if (any_pageable && !ctx->pool) {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        ctx->pool.reset(new (std::nothrow) CopyPool(std::min(16u, hw) - 1));
+    }
+    auto copy = [&](const std::vector<Piece>& p) {
+        if (ctx->pool)
+            ctx->pool->run(p);
+        else
+            for (const Piece& q : p) std::memcpy(q.dst, q.src, q.bytes);
+    };
+
+    const uint64_t nchunks = (n + chunk - 1) / chunk;
+    int64_t pending[fvb_ctx::kSlots];
+    for (auto& p : pending) p = -1;
+    std::vector<Piece> pieces;
+    // Unpack the pageable outputs of the chunk a slot last carried.
+    auto finish = [&](int slot) -> fvb_status {
+        if (pending[slot] < 0) return FVB_OK;
+        const uint64_t off = uint64_t(pending[slot]) * chunk;
+        const uint64_t cnt = std::min(chunk, n - off);
+        pending[slot] = -1;
+        const cudaError_t e = cudaEventSynchronize(ctx->done[slot]);
+        if (e != cudaSuccess) return cuda_fail(e, "pipeline chunk");
+        pieces.clear();
+        char* pin = static_cast<char*>(ctx->pin_buf[slot]);
+        for (const Arg& a : args)
+            if (a.out && a.host && a.has_pin)
+                add_pieces(pieces, a.host + off * a.width, pin + a.pin_off * chunk, cnt * a.width);
+        copy(pieces);
+        return FVB_OK;
+    };
+
+    std::vector<void*> dargs(args.size());
+    for (uint64_t c = 0; c < nchunks; ++c) {
+        const int slot = int(c % fvb_ctx::kSlots);
+        cudaStream_t s = ctx->stream[slot];
+        const uint64_t off = c * chunk;
+        const uint64_t cnt = std::min(chunk, n - off);
+        char* dbase = static_cast<char*>(ctx->slot_buf[slot]);
+        char* pin = static_cast<char*>(ctx->pin_buf[slot]);
+        if (fvb_status st = finish(slot)) return st;  // the bounce buffers are free again
+        // pack this chunk's pageable inputs
+        pieces.clear();
+        for (const Arg& a : args)
+            if (!a.out && a.host && a.has_pin)
+                add_pieces(pieces, pin + a.pin_off * chunk, a.host + off * a.width, cnt * a.width);
+        copy(pieces);
+        for (size_t i = 0; i < args.size(); ++i) {
+            const Arg& a = args[i];
+            if (a.dev) {
+                dargs[i] = a.dev + off * a.width;
+                continue;
+            }
+            if (a.scratch) {
+                dargs[i] = dbase + a.dev_off * chunk;
+                continue;
+            }
+            if (!a.host) {
+                dargs[i] = nullptr;
+                continue;
+            }
+            dargs[i] = dbase + a.dev_off * chunk;
+            if (a.out) continue;
+            const char* src = a.has_pin ? pin + a.pin_off * chunk : a.host + off * a.width;
+            const cudaError_t e =
+                cudaMemcpyAsync(dargs[i], src, cnt * a.width, cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess) return cuda_fail(e, "host->device copy");
+        }
+        if (fvb_status st = launch(dargs.data(), cnt, s)) return st;
+        bool unpack = false;
+        for (size_t i = 0; i < args.size(); ++i) {
+            const Arg& a = args[i];
+            if (!a.out || !a.host) continue;
+            char* dst = a.has_pin ? pin + a.pin_off * chunk : a.host + off * a.width;
+            unpack |= a.has_pin;
+            const cudaError_t e =
+                cudaMemcpyAsync(dst, dargs[i], cnt * a.width, cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) return cuda_fail(e, "device->host copy");
+        }
+        if (unpack) {
+            const cudaError_t e = cudaEventRecord(ctx->done[slot], s);
+            if (e != cudaSuccess) return cuda_fail(e, "chunk event");
+            pending[slot] = int64_t(c);
+        }
+    }
+    for (uint64_t c = nchunks > fvb_ctx::kSlots ? nchunks - fvb_ctx::kSlots : 0; c < nchunks; ++c)
+        if (fvb_status st = finish(int(c % fvb_ctx::kSlots))) return st;
+    for (int s = 0; s < fvb_ctx::kSlots; ++s) {
+        const cudaError_t e = cudaStreamSynchronize(ctx->stream[s]);
+        if (e != cudaSuccess) return cuda_fail(e, "pipeline completion");
+    }
+    return FVB_OK;
 }
 
 // Host threads copying pass-through items: output j < PASS is bit-for-bit
@@ -109,6 +396,26 @@ struct PassThrough {
     }
 };
 
+fvb_status reset_lambda(fvb_ctx* ctx, size_t bytes) {
+    cudaError_t e = cudaMemsetAsync(ctx->red, 0, bytes, ctx->stream[0]);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->reset_done, ctx->stream[0]);
+    for (int s = 1; s < fvb_ctx::kSlots && e == cudaSuccess; ++s)
+        e = cudaStreamWaitEvent(ctx->stream[s], ctx->reset_done, 0);
+    return e == cudaSuccess ? FVB_OK : cuda_fail(e, "lambda reset");
+}
+
+template <class T>
+fvb_status read_lambda(fvb_ctx* ctx, double* lambda_max) {
+    using Bu = typename Bits<T>::U;
+    Bu bits = 0;
+    const cudaError_t e = cudaMemcpy(&bits, ctx->red, sizeof(Bu), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "lambda_max read-back");
+    T v;
+    std::memcpy(&v, &bits, sizeof v);
+    *lambda_max = double(v);
+    return FVB_OK;
+}
+
 template <class Op, class T, bool RED, bool TUNE, int PASS = 0>
 fvb_status pipeline(fvb_ctx* ctx, const void* const* in, void* const* out, uint64_t n,
                     const Consts<T>& k, double* lambda_max) {
@@ -126,60 +433,32 @@ fvb_status pipeline(fvb_ctx* ctx, const void* const* in, void* const* out, uint6
         return fail(FVB_EARG, "host output plane overlaps an input plane");
     DeviceGuard guard(ctx->device);
     using Bu = typename Bits<T>::U;
-    if (RED) {
-        cudaError_t e = cudaMemsetAsync(ctx->red, 0, sizeof(Bu), ctx->stream[0]);
-        if (e == cudaSuccess) e = cudaEventRecord(ctx->reset_done, ctx->stream[0]);
-        for (int s = 1; s < fvb_ctx::kSlots && e == cudaSuccess; ++s)
-            e = cudaStreamWaitEvent(ctx->stream[s], ctx->reset_done, 0);
-        if (e != cudaSuccess) return cuda_fail(e, "lambda reset");
-    }
+    if (RED)
+        if (fvb_status st = reset_lambda(ctx, sizeof(Bu))) return st;
     if (n == 0) {
         if (RED && lambda_max) *lambda_max = 0.0;
         return FVB_OK;
     }
-    const uint64_t chunk = chunk_for(ctx, sizeof(T) * (NIN + NOUT), n);
-    if (fvb_status st = ensure_slots(ctx, size_t(chunk) * sizeof(T) * (NIN + NOUT))) return st;
-
+    std::vector<Arg> args;
+    for (int i = 0; i < NIN; ++i)
+        args.push_back({static_cast<char*>(const_cast<void*>(in[i])), nullptr, sizeof(T), false});
+    for (int j = 0; j < NOUT; ++j) {
+        // pass-through outputs are copied host-side; the kernel's copy of
+        // them lands in a device scratch slot
+        Arg a{j < PASS ? nullptr : static_cast<char*>(out[j]), nullptr, sizeof(T), true};
+        a.scratch = j < PASS;
+        args.push_back(a);
+    }
     PassThrough pass(in, out, PASS, size_t(n) * sizeof(T));
-    const uint64_t nchunks = (n + chunk - 1) / chunk;
-    for (uint64_t c = 0; c < nchunks; ++c) {
-        const int slot = int(c % fvb_ctx::kSlots);
-        cudaStream_t s = ctx->stream[slot];
-        const uint64_t off = c * chunk;
-        const uint64_t cnt = std::min(chunk, n - off);
-        const size_t bytes = size_t(cnt) * sizeof(T);
-        T* base = static_cast<T*>(ctx->slot_buf[slot]);
+    fvb_status st = staged(ctx, args, n, [&](void* const* d, uint64_t cnt, cudaStream_t s) {
         const T* din[NIN];
         T* dout[NOUT > 0 ? NOUT : 1];
-        for (int i = 0; i < NIN; ++i) {
-            T* d = base + size_t(i) * chunk;
-            din[i] = d;
-            const cudaError_t e = cudaMemcpyAsync(d, static_cast<const T*>(in[i]) + off, bytes,
-                                                  cudaMemcpyHostToDevice, s);
-            if (e != cudaSuccess) return cuda_fail(e, "host->device copy");
-        }
-        for (int j = 0; j < NOUT; ++j) dout[j] = base + size_t(NIN + j) * chunk;
-        fvb_status st = launch_op<Op, T, RED, TUNE>(din, dout, cnt, k,
-                                                    static_cast<Bu*>(ctx->red), s);
-        if (st) return st;
-        for (int j = PASS; j < NOUT; ++j) {
-            const cudaError_t e = cudaMemcpyAsync(static_cast<T*>(out[j]) + off, dout[j], bytes,
-                                                  cudaMemcpyDeviceToHost, s);
-            if (e != cudaSuccess) return cuda_fail(e, "device->host copy");
-        }
-    }
-    for (int s = 0; s < fvb_ctx::kSlots; ++s) {
-        const cudaError_t e = cudaStreamSynchronize(ctx->stream[s]);
-        if (e != cudaSuccess) return cuda_fail(e, "pipeline completion");
-    }
-    if (RED && lambda_max) {
-        Bu bits = 0;
-        const cudaError_t e = cudaMemcpy(&bits, ctx->red, sizeof(Bu), cudaMemcpyDeviceToHost);
-        if (e != cudaSuccess) return cuda_fail(e, "lambda_max read-back");
-        T v;
-        std::memcpy(&v, &bits, sizeof v);
-        *lambda_max = double(v);
-    }
+        for (int i = 0; i < NIN; ++i) din[i] = static_cast<const T*>(d[i]);
+        for (int j = 0; j < NOUT; ++j) dout[j] = static_cast<T*>(d[NIN + j]);
+        return launch_op<Op, T, RED, TUNE>(din, dout, cnt, k, static_cast<Bu*>(ctx->red), s);
+    });
+    if (st) return st;
+    if (RED && lambda_max) return read_lambda<T>(ctx, lambda_max);
     return FVB_OK;
 }
 
@@ -230,8 +509,10 @@ fvb_status fvb_ctx_create(int device, uint64_t chunk_points, fvb_ctx** out) {
     ctx->device = device;
     ctx->chunk_points = chunk_points;
     DeviceGuard guard(device);
-    for (int s = 0; s < fvb_ctx::kSlots && e == cudaSuccess; ++s)
+    for (int s = 0; s < fvb_ctx::kSlots && e == cudaSuccess; ++s) {
         e = cudaStreamCreateWithFlags(&ctx->stream[s], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->done[s], cudaEventDisableTiming);
+    }
     if (e == cudaSuccess) e = cudaMalloc(&ctx->red, 8);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->reset_done, cudaEventDisableTiming);
     if (e != cudaSuccess) {
@@ -248,6 +529,8 @@ fvb_status fvb_ctx_destroy(fvb_ctx* ctx) {
     for (int s = 0; s < fvb_ctx::kSlots; ++s) {
         if (ctx->stream[s]) cudaStreamSynchronize(ctx->stream[s]);
         if (ctx->slot_buf[s]) cudaFree(ctx->slot_buf[s]);
+        if (ctx->pin_buf[s]) cudaFreeHost(ctx->pin_buf[s]);
+        if (ctx->done[s]) cudaEventDestroy(ctx->done[s]);
         if (ctx->stream[s]) cudaStreamDestroy(ctx->stream[s]);
     }
     if (ctx->red) cudaFree(ctx->red);
@@ -279,6 +562,79 @@ fvb_status fvb_jacobian_host(fvb_ctx* ctx, const fvb_gas* gas, uint32_t dim, uin
         if (lambda_max)
             return pipeline_dim<JacobianOp, true, float>(ctx, gas, dim, in, out, n, lambda_max);
         return pipeline_dim<JacobianOp, false, float>(ctx, gas, dim, in, out, n, nullptr);
+    });
+}
+
+fvb_status fvb_launch_host(fvb_ctx* ctx, const fvb_kernel* k, uint64_t n, void* const* args,
+                           const uint8_t* arg_prec, const uint8_t* arg_on_device,
+                           double* lambda_max, void* after) {
+    return guarded([&]() -> fvb_status {
+        if (!ctx || !k || !args || !arg_prec) return fail(FVB_EARG, "NULL argument");
+        if (lambda_max && !k->reduce) return fail(FVB_EARG, "kernel has no CFL reduction");
+        const size_t nargs = size_t(k->n_outputs) + k->n_inputs;
+        if (nargs == 0) return fail(FVB_EARG, "kernel without arguments");
+        std::vector<Arg> v(nargs);
+        for (size_t i = 0; i < nargs; ++i) {
+            if (arg_prec[i] > 1) return fail(FVB_EPREC, "argument precision must be 0 or 1");
+            Arg& a = v[i];
+            a.width = arg_prec[i] ? 8 : 4;
+            a.out = i < k->n_outputs;
+            const uint8_t where = arg_on_device ? arg_on_device[i] : 0;
+            if (where == 2) {  // written on the device, never copied back
+                if (!a.out) return fail(FVB_EARG, "only an output slot can be discarded");
+                a.scratch = true;
+                continue;
+            }
+            if (!args[i]) {
+                if (!a.out) return fail(FVB_EARG, "NULL leaf plane");
+                continue;  // a NULL output slot (e.g. reduce-only wave speed)
+            }
+            if (where) {
+                a.dev = static_cast<char*>(args[i]);
+            } else {
+                a.host = static_cast<char*>(args[i]);
+            }
+        }
+        // In place: an output that is a host leaf shares its staging; any
+        // other overlap between host planes has no element-wise meaning.
+        for (size_t j = 0; j < k->n_outputs; ++j) {
+            Arg& o = v[j];
+            if (!o.host) continue;
+            const uintptr_t olo = uintptr_t(o.host), ohi = olo + n * o.width;
+            for (size_t i = 0; i < nargs; ++i) {
+                if (i == j || !v[i].host) continue;
+                const uintptr_t lo = uintptr_t(v[i].host), hi = lo + n * v[i].width;
+                if (lo == olo && v[i].width == o.width) {
+                    if (i >= k->n_outputs && o.alias < 0) o.alias = int(i);
+                    else if (i < k->n_outputs)
+                        return fail(FVB_EARG, "two host outputs name one plane");
+                } else if (lo < ohi && olo < hi && n > 0) {
+                    return fail(FVB_EARG, "host planes overlap at an offset");
+                }
+            }
+        }
+        DeviceGuard guard(ctx->device);
+        const size_t red_bytes = k->prec ? 8 : 4;  // the kernel's accumulator
+        if (lambda_max)
+            if (fvb_status st = reset_lambda(ctx, red_bytes)) return st;
+        if (after) {  // device work the caller queued first (producing resident planes)
+            cudaError_t e = cudaEventRecord(ctx->reset_done, static_cast<cudaStream_t>(after));
+            for (int s = 0; s < fvb_ctx::kSlots && e == cudaSuccess; ++s)
+                e = cudaStreamWaitEvent(ctx->stream[s], ctx->reset_done, 0);
+            if (e != cudaSuccess) return cuda_fail(e, "ordering after the caller's stream");
+        }
+        if (n == 0) {
+            if (lambda_max) *lambda_max = 0.0;
+            return FVB_OK;
+        }
+        fvb_status st = staged(ctx, v, n, [&](void* const* d, uint64_t cnt, cudaStream_t s) {
+            if (lambda_max) return k->reduce(k, 0, cnt, d, ctx->red, s);
+            return k->fn(k, 0, cnt, d, s);
+        });
+        if (st) return st;
+        if (lambda_max) return red_bytes == 8 ? read_lambda<double>(ctx, lambda_max)
+                                              : read_lambda<float>(ctx, lambda_max);
+        return FVB_OK;
     });
 }
 

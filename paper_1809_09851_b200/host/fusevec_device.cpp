@@ -14,6 +14,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <thread>
 
 #include "fvb.h"
 
@@ -231,26 +232,11 @@ struct Plan {
     fvb_kernel k{};
     std::vector<const DenseVector*> leaves;
     std::vector<Out> outs;
+    // Per output: the host leaf a bare-leaf item copies (the flux's row 0 is
+    // the momentum fields), when that copy can be made host-side instead of
+    // crossing PCIe twice; nullptr otherwise.  Set by block_impl.
+    std::vector<const DenseVector*> pass_src;
 };
-
-// Streams and staging memory reused across calls (per device).
-struct Staging {
-    cudaStream_t s[2] = {nullptr, nullptr};
-    void* buf[2] = {nullptr, nullptr};
-    std::size_t bytes = 0;
-};
-
-Staging& staging(int ordinal) {
-    static std::mutex mu;
-    static std::map<int, std::unique_ptr<Staging>> per;
-    std::lock_guard<std::mutex> lock(mu);
-    auto& p = per[ordinal];
-    if (!p) {
-        p = std::make_unique<Staging>();
-        for (auto& s : p->s) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-    }
-    return *p;
-}
 
 struct DeviceGuard {
     int prev = -1;
@@ -263,104 +249,131 @@ struct DeviceGuard {
     }
 };
 
-// Execute a plan over [0, n): resident leaves/outputs in place, host ones
-// staged through the device chunk by chunk on two alternating streams.
-// With red != nullptr the kernel's CFL reduction accumulates into it.
+// The C library's host-buffer context for one device: staging slots, pinned
+// bounce buffers for pageable DenseVectors and the copy threads
+// (fvb_launch_host).  The reference's backends are re-entrant -- evaluate()
+// may run on several host threads at once -- so staged evaluations on one
+// device take turns on it (each is bound by the PCIe link anyway).
+struct HostCtx {
+    std::mutex mu;
+    fvb_ctx* ctx = nullptr;
+};
+
+HostCtx& host_ctx(int ordinal) {
+    static std::mutex mu;
+    static std::map<int, std::unique_ptr<HostCtx>> per;
+    std::lock_guard<std::mutex> lock(mu);
+    auto& p = per[ordinal];
+    if (!p) p = std::make_unique<HostCtx>();
+    return *p;
+}
+
+// Host-side copies of pass-through items, on a few threads, running while
+// the device pipeline streams the computed items.  Joined on destruction.
+struct HostCopies {
+    std::vector<std::thread> threads;
+    explicit HostCopies(const std::vector<std::pair<DenseVector*, const DenseVector*>>& jobs) {
+        if (jobs.empty()) return;
+        std::size_t total = 0;
+        for (const auto& j : jobs) total += j.second->byte_size();
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const unsigned nt = std::min<unsigned>(4u, std::max(1u, hw / 4));
+        const std::size_t per = (total + nt - 1) / nt;
+        auto copy = [jobs](std::size_t lo, std::size_t hi) {
+            std::size_t base = 0;
+            for (const auto& [dst, src] : jobs) {
+                const std::size_t b = src->byte_size();
+                const std::size_t a = std::max(lo, base), e = std::min(hi, base + b);
+                if (a < e)
+                    std::memcpy(static_cast<char*>(dst->raw()) + (a - base),
+                                static_cast<const char*>(src->raw()) + (a - base), e - a);
+                base += b;
+            }
+        };
+        try {
+            for (unsigned t = 0; t < nt; ++t)
+                threads.emplace_back(copy, std::size_t(t) * per, std::min(total, (t + 1) * per));
+        } catch (...) {
+            for (auto& th : threads) th.join();
+            threads.clear();
+            copy(0, total);
+        }
+    }
+    ~HostCopies() {
+        for (auto& th : threads) th.join();
+    }
+};
+
+// Execute a plan over [0, n).  Device planes (resident leaves, device
+// destinations) are used in place; with every plane on the device it is one
+// launch on the backend's stream.  Otherwise fvb_launch_host streams the
+// range through the device in chunks, DMA-ing pinned host planes directly
+// and packing pageable ones through pinned bounce buffers.  With red !=
+// nullptr (a device scalar of the kernel's precision, zeroed) the kernel's
+// CFL reduction runs too and its result lands in *red.
 void run(const DeviceBackend& be, Plan& plan, std::size_t n, void* red) {
     if (n == 0) return;
-    // Per-slot element widths: a lowered kernel may mix f32 and f64 planes
-    // (the key carries each leaf's and each destination's precision); a
-    // hand-written kernel only ever matches uniform-precision keys.
-    std::vector<std::size_t> wl, wo;
-    for (const DenseVector* l : plan.leaves) wl.push_back(scalar_width(l->precision()));
-    for (const Out& o : plan.outs) wo.push_back(scalar_width(o.prec()));
-    constexpr std::size_t kSlotWidth = sizeof(double);  // staging slot stride per element
-
     DeviceGuard guard(be.ordinal);
-    // which leaves / outputs need staging
-    std::vector<void*> resident_leaf(plan.leaves.size(), nullptr);
-    std::size_t staged = 0;
-    for (std::size_t i = 0; i < plan.leaves.size(); ++i) {
-        DeviceVector* dv = be.residency ? be.residency->find(plan.leaves[i]) : nullptr;
-        if (dv) {
-            if (dv->size() != n || dv->precision() != plan.leaves[i]->precision())
+    const std::size_t nout = plan.outs.size(), nin = plan.leaves.size();
+    std::vector<void*> args(nout + nin, nullptr);
+    std::vector<uint8_t> prec(nout + nin, 1), on_dev(nout + nin, 0);
+    bool staged = false;
+    std::vector<std::pair<DenseVector*, const DenseVector*>> pass;
+    for (std::size_t j = 0; j < nout; ++j) {
+        const Out& o = plan.outs[j];
+        prec[j] = o.prec() == Precision::f64 ? 1 : 0;
+        if (j < plan.pass_src.size() && plan.pass_src[j]) {
+            on_dev[j] = 2;  // computed into device scratch only; copied host-side
+            pass.push_back({o.host, plan.pass_src[j]});
+            staged = true;
+        } else if (o.dev) {
+            args[j] = o.dev->data();
+            on_dev[j] = 1;
+        } else if (o.host) {
+            args[j] = o.host->raw();
+            staged = true;
+        }
+    }
+    for (std::size_t i = 0; i < nin; ++i) {
+        const DenseVector* l = plan.leaves[i];
+        prec[nout + i] = l->precision() == Precision::f64 ? 1 : 0;
+        if (DeviceVector* dv = be.residency ? be.residency->find(l) : nullptr) {
+            if (dv->size() != n || dv->precision() != l->precision())
                 throw LengthMismatch("resident plane does not match its host leaf");
-            resident_leaf[i] = dv->data();
+            args[nout + i] = dv->data();
+            on_dev[nout + i] = 1;
         } else {
-            ++staged;
+            args[nout + i] = const_cast<void*>(static_cast<const void*>(l->raw()));
+            staged = true;
         }
     }
-    // An output aliasing a staged leaf (in-place evaluate) reuses its buffer.
-    std::vector<long> alias(plan.outs.size(), -1);
-    for (std::size_t j = 0; j < plan.outs.size(); ++j) {
-        if (!plan.outs[j].host) continue;  // device planes and NULL slots need no staging
-        for (std::size_t i = 0; i < plan.leaves.size(); ++i)
-            if (plan.leaves[i] == plan.outs[j].host && !resident_leaf[i]) alias[j] = long(i);
-        if (alias[j] < 0) ++staged;
-    }
-
-    const bool external = be.stream != nullptr;
-    Staging& st = staging(be.ordinal);
-    std::size_t chunk = staged ? std::max<std::size_t>(be.chunk_points & ~std::size_t(63), 64) : n;
-    chunk = std::min(chunk, n);
-    const std::size_t need = staged * chunk * kSlotWidth;
-    if (need > st.bytes) {
-        for (int b = 0; b < 2; ++b) {
-            if (st.buf[b]) {
-                cuda_check(cudaStreamSynchronize(st.s[b]), "staging drain");
-                cuda_check(cudaFree(st.buf[b]), "cudaFree");
-                st.buf[b] = nullptr;
-            }
-            cuda_check(cudaMalloc(&st.buf[b], need), "staging allocation");
-        }
-        st.bytes = need;
-    }
-
-    std::vector<void*> args(plan.outs.size() + plan.leaves.size());
-    for (std::size_t off = 0, c = 0; off < n; off += chunk, ++c) {
-        const std::size_t cnt = std::min(chunk, n - off);
-        const int b = external ? 0 : int(c % 2);
-        cudaStream_t s = external ? static_cast<cudaStream_t>(be.stream) : st.s[b];
-        char* base = static_cast<char*>(st.buf[b]);
-        std::size_t slot = 0;
-        std::vector<void*> leaf_ptr(plan.leaves.size());
-        for (std::size_t i = 0; i < plan.leaves.size(); ++i) {
-            if (resident_leaf[i]) {
-                leaf_ptr[i] = static_cast<char*>(resident_leaf[i]) + off * wl[i];
-            } else {
-                leaf_ptr[i] = base + (slot++) * chunk * kSlotWidth;
-                cuda_check(cudaMemcpyAsync(leaf_ptr[i],
-                                           static_cast<const char*>(plan.leaves[i]->raw()) + off * wl[i],
-                                           cnt * wl[i], cudaMemcpyHostToDevice, s),
-                           "host->device copy");
-            }
-        }
-        for (std::size_t j = 0; j < plan.outs.size(); ++j) {
-            if (plan.outs[j].is_null())
-                args[j] = nullptr;
-            else if (plan.outs[j].dev)
-                args[j] = static_cast<char*>(plan.outs[j].dev->data()) + off * wo[j];
-            else if (alias[j] >= 0)
-                args[j] = leaf_ptr[std::size_t(alias[j])];
-            else
-                args[j] = base + (slot++) * chunk * kSlotWidth;
-        }
-        for (std::size_t i = 0; i < plan.leaves.size(); ++i) args[plan.outs.size() + i] = leaf_ptr[i];
+    cudaStream_t s = static_cast<cudaStream_t>(be.stream);
+    if (!staged) {
         if (red)
-            fvb_check(plan.k.reduce(&plan.k, 0, cnt, args.data(), red, s));
+            fvb_check(plan.k.reduce(&plan.k, 0, n, args.data(), red, s));
         else
-            fvb_check(plan.k.fn(&plan.k, 0, cnt, args.data(), s));
-        for (std::size_t j = 0; j < plan.outs.size(); ++j)
-            if (plan.outs[j].host)
-                cuda_check(cudaMemcpyAsync(static_cast<char*>(plan.outs[j].host->raw()) + off * wo[j],
-                                           args[j], cnt * wo[j], cudaMemcpyDeviceToHost, s),
-                           "device->host copy");
+            fvb_check(plan.k.fn(&plan.k, 0, n, args.data(), s));
+        cuda_check(cudaStreamSynchronize(s), "sync");
+        return;
     }
-    if (external) {
-        cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(be.stream)), "sync");
-    } else {
-        cuda_check(cudaStreamSynchronize(st.s[0]), "sync");
-        cuda_check(cudaStreamSynchronize(st.s[1]), "sync");
+    HostCtx& hc = host_ctx(be.ordinal);
+    std::lock_guard<std::mutex> lock(hc.mu);
+    if (!hc.ctx) fvb_check(fvb_ctx_create(be.ordinal, be.chunk_points, &hc.ctx));
+    double lam = 0.0;
+    fvb_status st;
+    {
+        HostCopies copies(pass);  // joined before the result is returned
+        st = fvb_launch_host(hc.ctx, &plan.k, n, args.data(), prec.data(), on_dev.data(),
+                             red ? &lam : nullptr, be.stream);
+    }
+    fvb_check(st);
+    if (red) {  // hand the maximum back through the caller's device scalar
+        if (plan.k.prec) {
+            cuda_check(cudaMemcpy(red, &lam, sizeof lam, cudaMemcpyHostToDevice), "lambda");
+        } else {
+            const float f = static_cast<float>(lam);
+            cuda_check(cudaMemcpy(red, &f, sizeof f, cudaMemcpyHostToDevice), "lambda");
+        }
     }
 }
 
@@ -620,6 +633,22 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
     }
     if (need_reduce && !plan.k.reduce)
         throw UnsupportedExpression("block has no fused CFL reduction");
+    if (copies.empty() && plan.outs.size() == items.size()) {
+        // bare-leaf items of a fused block whose source and destination are
+        // both host vectors of one precision, and whose source no item
+        // overwrites: copied host-side while the device pipeline runs
+        plan.pass_src.assign(plan.outs.size(), nullptr);
+        for (std::size_t j = 0; j < items.size(); ++j) {
+            const DenseVector* src = bare_leaf(items[j].node());
+            const Out& o = plan.outs[j];
+            if (!src || !o.host || o.host->precision() != src->precision() ||
+                (be.residency && be.residency->find(src)))
+                continue;
+            bool written = false;
+            for (const Out& w : plan.outs) written |= w.host == src;
+            if (!written) plan.pass_src[j] = src;
+        }
+    }
     run(be, plan, n, red);
     for (auto& [src, d] : copies) {
         DeviceGuard guard(be.ordinal);

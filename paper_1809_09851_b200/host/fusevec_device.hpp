@@ -104,7 +104,7 @@ struct DeviceBackend {
     int ordinal = 0;
     void* stream = nullptr;              // cudaStream_t; nullptr = legacy default
     const Residency* residency = nullptr;
-    std::size_t chunk_points = 1u << 22;  // staging granularity for host buffers
+    std::size_t chunk_points = 0;  // host-buffer staging chunk (0 = 256 MiB of device staging per slot)
 };
 
 /// UETLI tie: a list of device destinations a multi-output block writes in

@@ -20,7 +20,9 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <chrono>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "fusevec/block.hpp"
@@ -672,6 +674,37 @@ void run_gpu() {
         return "kernel " + name;
     });
 
+    check("re-entrant: 4 host threads evaluate different blocks at once", [&] {
+        // The reference's backends are stateless and re-entrant
+        // (proj/src/backend_eval.cpp:280-346); the device path shares staging
+        // buffers per device and must stay correct under concurrent callers.
+        const std::size_t n = 300000;
+        std::vector<std::string> errs(4);
+        std::vector<std::thread> pool;
+        for (int t = 0; t < 4; ++t)
+            pool.emplace_back([&, t] {
+                try {
+                    SplitMix64 rng(0xD0 + t);
+                    const std::size_t d = 1 + t % 3;
+                    auto f = random_state(d, n, rng);
+                    StateSet u = state_conservative(EosSpec(), d, leaves_of(f));
+                    BlockVectorGrid want(d + 2, d, Precision::f64, n), got(d + 2, d, Precision::f64, n);
+                    evaluate_block(Backend::scalar_ref(), inviscid_flux(u), want);
+                    for (int rep = 0; rep < 3; ++rep) {
+                        dev::evaluate_block(be, inviscid_flux(u), got);
+                        for (std::size_t i = 0; i < (d + 2) * d; ++i)
+                            if (!same_bits(want.get(i), got.get(i))) throw std::runtime_error("differs");
+                    }
+                } catch (const std::exception& e) {
+                    errs[t] = e.what();
+                }
+            });
+        for (auto& th : pool) th.join();
+        for (int t = 0; t < 4; ++t)
+            if (!errs[t].empty()) fail("thread " + std::to_string(t) + ": " + errs[t]);
+        return "";
+    });
+
     check("errors: unsupported expression, length/shape mismatch, tag conflict, empty tree", [&] {
         DenseVector a(Precision::f64, 10), b(Precision::f64, 11), out(Precision::f64, 10);
         bool threw = false;
@@ -732,8 +765,55 @@ void run_gpu() {
 
 }  // namespace
 
+// The reference-facing plugin with host DenseVectors (pageable memory, as
+// the reference allocates them) and with device-resident leaves: 3-D flux,
+// fp64, timed with a host clock around whole evaluate_block calls.
+void run_perf(std::size_t n) {
+    dev::DeviceBackend be;
+    SplitMix64 rng(0x5EED);
+    auto f = random_state(3, n, rng);
+    StateSet u = state_conservative(EosSpec(), 3, leaves_of(f));
+    BlockVectorGrid grid(5, 3, Precision::f64, n);
+    auto time = [&](const dev::DeviceBackend& b, const char* what) {
+        dev::evaluate_block(b, inviscid_flux(u), grid);  // warm (allocations, key)
+        const int reps = 3;
+        auto t0 = std::chrono::steady_clock::now();
+        for (int r = 0; r < reps; ++r) dev::evaluate_block(b, inviscid_flux(u), grid);
+        const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / reps;
+        std::printf("{\"path\": \"%s\", \"points\": %zu, \"ms\": %.3f, \"gpts\": %.4f}\n", what, n,
+                    s * 1e3, n / s / 1e9);
+        std::fflush(stdout);
+    };
+    time(be, "evaluate_block, host DenseVectors (pageable) in and out");
+    std::vector<dev::DeviceVector> dv;
+    dev::Residency res;
+    for (auto& v : f) {
+        dv.emplace_back(v.precision(), v.size());
+        dv.back().upload(v);
+    }
+    for (std::size_t i = 0; i < f.size(); ++i) res.bind(f[i], dv[i]);
+    dev::DeviceBackend rb = be;
+    rb.residency = &res;
+    time(rb, "evaluate_block, resident leaves, host grid out");
+    std::vector<dev::DeviceVector> outs;
+    for (int i = 0; i < 15; ++i) outs.emplace_back(Precision::f64, n);
+    dev::Tie tie;
+    for (auto& o : outs) tie.dests.push_back(&o);
+    dev::evaluate_block(rb, inviscid_flux(u), tie);
+    const int reps = 10;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < reps; ++r) dev::evaluate_block(rb, inviscid_flux(u), tie);
+    const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / reps;
+    std::printf("{\"path\": \"evaluate_block, resident leaves, tie'd device outputs\", \"points\": %zu, "
+                "\"ms\": %.3f, \"gpts\": %.4f}\n", n, s * 1e3, n / s / 1e9);
+}
+
 int main(int argc, char** argv) {
     const std::string mode = argc > 1 ? argv[1] : "keys";
+    if (mode == "perf") {
+        run_perf(argc > 2 ? std::strtoull(argv[2], nullptr, 10) : 20000000ull);
+        return 0;
+    }
     if (mode == "keys" || mode == "all") run_keys();
     if (mode == "gpu" || mode == "all") run_gpu();
     std::printf(failures ? "%d check(s) failed\n" : "all checks passed\n", failures);

@@ -327,6 +327,83 @@ def test_host_path_matches_device(cuda, orc, pinned):
     ctx.close()
 
 
+def _flux_kernel():
+    import re
+    import struct
+    pat = dict(fvb.patterns())["flux3_f64"]
+    return fvb.lookup(re.sub(r"Cd#(\w+);", lambda m: "Cd%016x;" % struct.unpack(
+        "<Q", struct.pack("<d", {"half": 0.5, "gm1": 0.4}[m.group(1)]))[0], pat))
+
+
+@pytest.mark.parametrize("mode", ["pageable", "pinned", "mixed"])
+def test_launch_host_any_kernel(cuda, orc, mode):
+    # fvb_launch_host: a structural-key kernel over host arrays -- pageable
+    # (bounced through pinned buffers by the copy threads), pinned (DMA'd
+    # directly) or a mix with device-resident leaves and device outputs --
+    # over several chunks; bitwise the oracle.
+    dim, n = 3, 1_000_003
+    s_np = orc.random_state(dim, n, seed=13)
+    want = orc.flux(dim, s_np)
+    k = _flux_kernel()
+    ctx = fvb.HostContext(0, chunk_points=1 << 18)
+    leaves = [None] * k.n_inputs
+    for ci in range(k.n_inputs):
+        leaves[k.in_slot[ci]] = torch.from_numpy(s_np[ci])
+    outs = [torch.empty(n, dtype=torch.float64) for _ in range(15)]
+    on_dev = [0] * (15 + k.n_inputs)
+    if mode == "pinned":
+        leaves = [t.pin_memory() for t in leaves]
+        outs = [t.pin_memory() for t in outs]
+    elif mode == "mixed":
+        for i in (0, 2):
+            leaves[i] = leaves[i].to(cuda)
+            on_dev[15 + i] = 1
+        for j in (1, 7):
+            outs[j] = torch.empty(n, dtype=torch.float64, device=cuda)
+            on_dev[j] = 1
+    args = N.ptr_array([t.data_ptr() for t in outs + leaves])
+    prec = (ctypes.c_uint8 * len(on_dev))(*([1] * len(on_dev)))
+    dev = (ctypes.c_uint8 * len(on_dev))(*on_dev)
+    N.check(N.lib().fvb_launch_host(ctx._h, ctypes.byref(k), n, args, prec, dev, None, None))
+    assert all_same([t.cpu().numpy() for t in outs], want)
+    # in place: pressure written over its own (pageable) rhoE leaf
+    import re
+    import struct
+    pat = dict(fvb.patterns())["pressure3_f64"]
+    kp = fvb.lookup(re.sub(r"Cd#(\w+);", lambda m: "Cd%016x;" % struct.unpack(
+        "<Q", struct.pack("<d", {"half": 0.5, "gm1": 0.4}[m.group(1)]))[0], pat))
+    hs = [torch.from_numpy(a.copy()) for a in s_np]
+    lv = [None] * kp.n_inputs
+    for ci in range(kp.n_inputs):
+        lv[kp.in_slot[ci]] = hs[ci]
+    args = N.ptr_array([hs[4].data_ptr()] + [t.data_ptr() for t in lv])
+    prec = (ctypes.c_uint8 * (1 + kp.n_inputs))(*([1] * (1 + kp.n_inputs)))
+    N.check(N.lib().fvb_launch_host(ctx._h, ctypes.byref(kp), n, args, prec, None, None, None))
+    assert same_bits(hs[4].numpy(), orc.cons2prim(dim, s_np)[dim])
+    # the CFL reduction with a NULL output slot (reduce only), host leaves
+    pat = dict(fvb.patterns())["wave_speed3_f64"]
+    kw = fvb.lookup(re.sub(r"Cd#(\w+);", lambda m: "Cd%016x;" % struct.unpack(
+        "<Q", struct.pack("<d", {"half": 0.5, "gm1": 0.4, "gamma": 1.4}[m.group(1)]))[0], pat))
+    lv = [None] * kw.n_inputs
+    for ci in range(kw.n_inputs):
+        lv[kw.in_slot[ci]] = torch.from_numpy(s_np[ci])
+    args = N.ptr_array([0] + [t.data_ptr() for t in lv])
+    prec = (ctypes.c_uint8 * (1 + kw.n_inputs))(*([1] * (1 + kw.n_inputs)))
+    lam = ctypes.c_double()
+    N.check(N.lib().fvb_launch_host(ctx._h, ctypes.byref(kw), n, args, prec, None,
+                                    ctypes.byref(lam), None))
+    assert lam.value == orc.wave_speed_max(dim, s_np)
+    # overlapping host planes at an offset are refused
+    buf = torch.empty(n + 8, dtype=torch.float64)
+    bad = [buf[:n], buf[3:n + 3]] + [torch.empty(n, dtype=torch.float64) for _ in range(13)]
+    args = N.ptr_array([t.data_ptr() for t in bad + [torch.from_numpy(a) for a in s_np]])
+    prec = (ctypes.c_uint8 * 20)(*([1] * 20))
+    with pytest.raises(fvb.ArgumentError):
+        N.check(N.lib().fvb_launch_host(ctx._h, ctypes.byref(k), n, args, prec, None, None,
+                                        None))
+    ctx.close()
+
+
 # ---- structural-key kernels -----------------------------------------------------------
 
 
