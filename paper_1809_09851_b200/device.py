@@ -309,6 +309,34 @@ class HostContext:
                                       N.ptr_array(outs)))
         return out
 
+    def launch(self, kernel, planes, n, reduce=False, after=None):
+        """fvb_launch_host: run a structural-key kernel (lookup()) over
+        `planes` -- its argument block, outputs then leaves in slot order.
+        Each plane is a 1-D tensor (CPU: pinned or pageable; CUDA: used in
+        place) or None for a NULL output slot.  Returns lambda_max when
+        `reduce` (the kernel's CFL reduction)."""
+        count = kernel.n_outputs + kernel.n_inputs
+        if len(planes) != count:
+            raise N.ArgumentError(N.FVB_EARG, f"kernel takes {count} planes, got {len(planes)}")
+        ptrs, prec, dev = [], [], []
+        for t in planes:
+            if t is None:
+                ptrs.append(0)
+                prec.append(1)
+                dev.append(0)
+                continue
+            if t.dim() != 1 or not t.is_contiguous() or t.numel() != n:
+                raise N.ArgumentError(N.FVB_EARG, "planes must be contiguous 1-D of length n")
+            ptrs.append(t.data_ptr())
+            prec.append(_PREC[t.dtype])
+            dev.append(1 if t.is_cuda else 0)
+        lam = ctypes.c_double()
+        N.check(N.lib().fvb_launch_host(
+            self._h, ctypes.byref(kernel), n, N.ptr_array(ptrs), (ctypes.c_uint8 * count)(*prec),
+            (ctypes.c_uint8 * count)(*dev), ctypes.byref(lam) if reduce else None,
+            _stream(after) if after is not None else None))
+        return lam.value if reduce else None
+
     def jacobian(self, state, dim, out, gas=None):
         ins, n, prec = self._host(state, "state")
         outs, _, _ = self._host(out, "out", n, prec)

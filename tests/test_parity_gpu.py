@@ -387,12 +387,8 @@ def test_launch_host_any_kernel(cuda, orc, mode):
     lv = [None] * kw.n_inputs
     for ci in range(kw.n_inputs):
         lv[kw.in_slot[ci]] = torch.from_numpy(s_np[ci])
-    args = N.ptr_array([0] + [t.data_ptr() for t in lv])
-    prec = (ctypes.c_uint8 * (1 + kw.n_inputs))(*([1] * (1 + kw.n_inputs)))
-    lam = ctypes.c_double()
-    N.check(N.lib().fvb_launch_host(ctx._h, ctypes.byref(kw), n, args, prec, None,
-                                    ctypes.byref(lam), None))
-    assert lam.value == orc.wave_speed_max(dim, s_np)
+    # (through the HostContext.launch wrapper; a None plane is a NULL slot)
+    assert ctx.launch(kw, [None] + lv, n, reduce=True) == orc.wave_speed_max(dim, s_np)
     # overlapping host planes at an offset are refused
     buf = torch.empty(n + 8, dtype=torch.float64)
     bad = [buf[:n], buf[3:n + 3]] + [torch.empty(n, dtype=torch.float64) for _ in range(13)]
