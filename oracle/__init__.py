@@ -85,7 +85,22 @@ class Oracle:
         L.fvo_wave_speed_f64.argtypes = [GasC, i32, u64, pp, vp]
         L.fvo_eos_p_f64.argtypes = [GasC, u64, vp, vp, vp]
         L.fvo_eos_T_f64.argtypes = [GasC, u64, vp, vp]
+        for yx in ("yd_xd", "yd_xs", "ys_xd", "ys_xs"):
+            getattr(L, f"fvo_csr_matvec_acc_{yx}").argtypes = [u64, vp, vp, vp, vp, vp]
         self.L = L
+
+    def csr_matvec_acc(self, rp, ci, v, x, y):
+        """y += A x in y's precision, rows summed in stored order
+        (block.cpp:345-356).  rp/ci uint64, v float64; returns the new y."""
+        y = np.array(y, copy=True)
+        yx = ("yd" if y.dtype == np.float64 else "ys") + "_" + \
+             ("xd" if x.dtype == np.float64 else "xs")
+        rp = np.ascontiguousarray(rp, np.uint64)
+        ci = np.ascontiguousarray(ci, np.uint64)
+        v = np.ascontiguousarray(v, np.float64)
+        getattr(self.L, f"fvo_csr_matvec_acc_{yx}")(len(rp) - 1, rp.ctypes.data, ci.ctypes.data,
+                                                     v.ctypes.data, x.ctypes.data, y.ctypes.data)
+        return y
 
     @staticmethod
     def gas(cp=(7, 2), cv=(5, 2)) -> GasC:
@@ -186,7 +201,31 @@ class Reference:
         L.fvr_wave_speed.argtypes = [gas, i32, i32, u64, pp, vp, ctypes.POINTER(dbl), i32]
         L.fvr_time_config.argtypes = [i32, i32, i32, u64, i32, i32, u64, ctypes.POINTER(dbl)]
         L.fvr_run_miniapp.argtypes = [i32, u64, i32, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]
+        L.fvr_csr_matvec.argtypes = [i32, i32, i32, u64, u64, vp, vp, vp, vp, vp, vp]
+        L.fvr_time_csr.argtypes = [u64, i32, ctypes.POINTER(dbl), ctypes.POINTER(u64)]
         self.L = L
+
+    def csr_matvec(self, rp, ci, v, x, cols, y_prec="f64", m_prec="f64"):
+        """y = A x through the reference's block_matvec / evaluate_block.
+        Returns (y, the values as SparseMatrix stores them)."""
+        rp = np.ascontiguousarray(rp, np.uint64)
+        ci = np.ascontiguousarray(ci, np.uint64)
+        v = np.ascontiguousarray(v, np.float64)
+        rows = len(rp) - 1
+        y = np.empty(rows, _DT[y_prec])
+        stored = np.empty(len(v), np.float64)
+        self._ok(self.L.fvr_csr_matvec(_PREC[y_prec], _PREC[_prec_of(x)], _PREC[m_prec], rows,
+                                       cols, rp.ctypes.data, ci.ctypes.data, v.ctypes.data,
+                                       x.ctypes.data, y.ctypes.data, stored.ctypes.data))
+        return y, stored
+
+    def time_csr(self, n, reps):
+        """Seconds per y = A x of the 7-point Laplacian on an n^3 grid
+        (serial, as the reference's csr_matvec_acc is), and its nnz."""
+        t = (ctypes.c_double * reps)()
+        nnz = ctypes.c_uint64()
+        self._ok(self.L.fvr_time_csr(n, reps, t, ctypes.byref(nnz)))
+        return [x * 1e-9 for x in t], nnz.value
 
     def _ok(self, rc):
         if rc != 0:

@@ -71,3 +71,20 @@ void fvo_wave_speed_f64(fvo_gas g, int dim, uint64_t n, const double* const* in,
         out[i] = lambda_at_f64(g.gm1, g.gamma, dim, rho, m, rho_E);
     }
 }
+
+/* csr_matvec_acc_t<TY, TX> (proj/src/block.cpp:345-356). */
+#define FVO_CSR(NAME, TY, TX)                                                          \
+    void NAME(uint64_t rows, const uint64_t* rp, const uint64_t* ci, const double* v,   \
+              const TX* x, TY* y) {                                                    \
+        for (uint64_t r = 0; r < rows; ++r) {                                          \
+            TY acc = 0;                                                                \
+            for (uint64_t k = rp[r]; k < rp[r + 1]; ++k)                               \
+                acc += (TY)v[k] * (TY)x[ci[k]];                                        \
+            y[r] += acc;                                                               \
+        }                                                                              \
+    }
+FVO_CSR(fvo_csr_matvec_acc_yd_xd, double, double)
+FVO_CSR(fvo_csr_matvec_acc_yd_xs, double, float)
+FVO_CSR(fvo_csr_matvec_acc_ys_xd, float, double)
+FVO_CSR(fvo_csr_matvec_acc_ys_xs, float, float)
+#undef FVO_CSR

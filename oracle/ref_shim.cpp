@@ -394,6 +394,68 @@ int fvr_time_config(int which, int dim, int prec, std::uint64_t n, int workers, 
     });
 }
 
+// y = A x through the reference's block layer: a 1x1 BlockMatrixView of the
+// CSR matrix (rows given as sorted, duplicate-free triplets, which the
+// SparseMatrix constructor stores unchanged: block.cpp:15-48) applied with
+// block_matvec and evaluate_block (block.cpp:264-298, 428-446), i.e.
+// y[r] = 0 + csr_matvec_acc row r.  v_stored receives the stored values
+// (narrowed to prec_m, block.cpp:45) when not NULL.
+int fvr_csr_matvec(int prec_y, int prec_x, int prec_m, std::uint64_t rows, std::uint64_t cols,
+                   const std::uint64_t* rp, const std::uint64_t* ci, const double* v,
+                   const void* x, void* y, double* v_stored) {
+    return guarded([&] {
+        std::vector<Triplet> trips;
+        trips.reserve(rows ? rp[rows] : 0);
+        for (std::uint64_t r = 0; r < rows; ++r)
+            for (std::uint64_t k = rp[r]; k < rp[r + 1]; ++k)
+                trips.push_back({std::size_t(r), std::size_t(ci[k]), v[k]});
+        SparseMatrix a(rows, cols, trips, prec_of(prec_m));
+        if (v_stored && !a.values().empty())
+            std::memcpy(v_stored, a.values().data(), a.values().size() * sizeof(double));
+        DenseVector xv = upload(prec_of(prec_x), cols, x);
+        std::vector<DenseVector> yv;
+        yv.emplace_back(prec_of(prec_y), rows);
+        BlockColVector out(std::move(yv));
+        BlockMatrixView view(1, 1, {&a});
+        evaluate_block(Backend::scalar_ref(), block_matvec(view, BlockExpr(1, 1, {BlockItem(xv)})),
+                       out);
+        download(out.get(0), y);
+    });
+}
+
+// The 7-point Laplacian on an n^3 grid (the PDE stencil the block layer's
+// matvec serves), y = A x timed through evaluate_block as above.  The
+// reference's csr_matvec_acc is serial whatever the backend.
+int fvr_time_csr(std::uint64_t n, int reps, double* times_ns, std::uint64_t* nnz_out) {
+    return guarded([&] {
+        const std::uint64_t rows = n * n * n;
+        std::vector<Triplet> trips;
+        trips.reserve(rows * 7);
+        const long long off[7] = {-(long long)(n * n), -(long long)n, -1, 0, 1, (long long)n,
+                                  (long long)(n * n)};
+        for (std::uint64_t r = 0; r < rows; ++r) {
+            const std::uint64_t i = r % n, j = (r / n) % n, k = r / (n * n);
+            const bool ok[7] = {k > 0, j > 0, i > 0, true, i + 1 < n, j + 1 < n, k + 1 < n};
+            for (int t = 0; t < 7; ++t)
+                if (ok[t]) trips.push_back({std::size_t(r), std::size_t((long long)r + off[t]),
+                                            t == 3 ? 6.0 : -1.0});
+        }
+        SparseMatrix a(rows, rows, trips);
+        *nnz_out = a.nnz();
+        SplitMix64 rng(7);
+        DenseVector xv(Precision::f64, rows);
+        for (std::uint64_t i = 0; i < rows; ++i) xv.set(i, rng.uniform(-1.0, 1.0));
+        std::vector<DenseVector> yv;
+        yv.emplace_back(Precision::f64, rows);
+        BlockColVector out(std::move(yv));
+        BlockMatrixView view(1, 1, {&a});
+        BlockExpr e = block_matvec(view, BlockExpr(1, 1, {BlockItem(xv)}));
+        evaluate_block(Backend::scalar_ref(), e, out);
+        for (int r = 0; r < reps; ++r)
+            times_ns[r] = time_ns([&] { evaluate_block(Backend::scalar_ref(), e, out); });
+    });
+}
+
 // The reference's own benchmark record (run_miniapp, proj/src/bench.cpp:294-384).
 int fvr_run_miniapp(int prec, std::uint64_t n, int workers, double* median_ns,
                     double* overhead_ratio) {

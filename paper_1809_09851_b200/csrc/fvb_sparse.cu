@@ -5,15 +5,23 @@
 //     acc = 0;  for k in row r (stored, column-sorted order):
 //         acc += (TY)v[k] * (TY)x[ci[k]];
 //     y[r] += acc;
-// in the destination's precision TY.  One thread owns one row and walks its
-// nonzeros in stored order, so the sum associates exactly as the reference's
-// does and the result is bitwise identical (--fmad=false keeps the multiply
-// and the add separately rounded).  Row-parallel, not nonzero-parallel: the
-// reference's block matrices are short-row (PDE stencils); the order of the
-// additions is the contract.
+// in the destination's precision TY.  The additions of one row must happen
+// in stored order (that is the bitwise contract), but the products are
+// independent: each is the same two roundings whichever thread computes it.
+//
+// So a warp owns 32 consecutive rows, whose nonzeros are one contiguous
+// range of the CSR arrays.  The warp streams that range in tiles of
+// kTile entries with coalesced loads (lane l takes entries l, l+32, ...),
+// computes every product once and parks it in shared memory; then each lane
+// adds up the products of its own row, in order, carrying acc from tile to
+// tile.  Values and column indices -- 16 of the ~20 bytes per nonzero --
+// are read as full 128-byte lines instead of one scattered word per row per
+// thread, and the sum associates exactly as the reference's
+// (--fmad=false keeps the multiply and the add separately rounded).
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "fvb.h"
 #include "fvb_dispatch.cuh"
@@ -21,9 +29,14 @@
 namespace fvb {
 namespace {
 
+constexpr int kCsrThreads = 256;
+constexpr int kTile = 256;  // products staged per warp per round
+
+// Row per thread, nonzeros walked in stored order (the simple form; kept for
+// the comparison in tools/csr_bench.py via FVB_CSR_ROWWISE=1).
 template <class TY, class TX>
-__global__ void __launch_bounds__(256)
-    csr_acc_kernel(uint64_t rows, const uint64_t* __restrict__ rp, const uint64_t* __restrict__ ci,
+__global__ void __launch_bounds__(kCsrThreads)
+    csr_row_kernel(uint64_t rows, const uint64_t* __restrict__ rp, const uint64_t* __restrict__ ci,
                    const double* __restrict__ v, const TX* __restrict__ x, TY* __restrict__ y) {
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < rows; r += stride) {
@@ -35,11 +48,63 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Warp-staged: see the file comment.  One warp per 32 rows, grid-stride.
+template <class TY, class TX>
+__global__ void __launch_bounds__(kCsrThreads)
+    csr_warp_kernel(uint64_t rows, const uint64_t* __restrict__ rp,
+                    const uint64_t* __restrict__ ci, const double* __restrict__ v,
+                    const TX* __restrict__ x, TY* __restrict__ y) {
+    __shared__ TY prod[kCsrThreads / 32][kTile];
+    const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    TY* p = prod[wib];
+    const uint64_t warps = uint64_t(gridDim.x) * (kCsrThreads / 32);
+    for (uint64_t w = uint64_t(blockIdx.x) * (kCsrThreads / 32) + wib; w * 32 < rows; w += warps) {
+        const uint64_t r = w * 32 + lane;
+        const bool valid = r < rows;
+        const uint64_t beg = valid ? rp[r] : 0;
+        const uint64_t end = valid ? rp[r + 1] : 0;
+        const uint64_t last = rows - w * 32 < 32 ? rows - w * 32 - 1 : 31;
+        const uint64_t B = __shfl_sync(0xffffffffu, beg, 0);
+        const uint64_t E = __shfl_sync(0xffffffffu, end, unsigned(last));
+        TY acc = 0;
+        for (uint64_t base = B; base < E; base += kTile) {
+            const uint64_t lim = E - base < uint64_t(kTile) ? E - base : uint64_t(kTile);
+#pragma unroll 4
+            for (uint64_t t = lane; t < lim; t += 32)
+                p[t] = static_cast<TY>(v[base + t]) * static_cast<TY>(x[ci[base + t]]);
+            __syncwarp();
+            const uint64_t lo = beg > base ? beg : base;
+            const uint64_t hi = end < base + lim ? end : base + lim;
+            for (uint64_t k = lo; k < hi; ++k) acc = acc + p[k - base];
+            __syncwarp();
+        }
+        if (valid) y[r] = y[r] + acc;
+    }
+}
+
+bool rowwise() {
+    static const bool v = [] {
+        const char* e = std::getenv("FVB_CSR_ROWWISE");
+        return e && *e && *e != '0';
+    }();
+    return v;
+}
+
 template <class TY, class TX>
 fvb_status launch_csr(uint64_t rows, const uint64_t* rp, const uint64_t* ci, const double* v,
                       const void* x, void* y, cudaStream_t s) {
-    csr_acc_kernel<TY, TX><<<simple_grid(rows), 256, 0, s>>>(
-        rows, rp, ci, v, static_cast<const TX*>(x), static_cast<TY*>(y));
+    if (rowwise()) {
+        csr_row_kernel<TY, TX><<<simple_grid(rows), kCsrThreads, 0, s>>>(
+            rows, rp, ci, v, static_cast<const TX*>(x), static_cast<TY*>(y));
+    } else {
+        // one pass over the rows: a warp per 32 rows, capped at a few waves
+        const uint64_t warps = (rows + 31) / 32;
+        uint64_t grid = (warps + kCsrThreads / 32 - 1) / (kCsrThreads / 32);
+        const uint64_t cap = uint64_t(device_sm_count()) * 8 * 64;
+        grid = grid < cap ? grid : cap;
+        csr_warp_kernel<TY, TX><<<unsigned(grid ? grid : 1), kCsrThreads, 0, s>>>(
+            rows, rp, ci, v, static_cast<const TX*>(x), static_cast<TY*>(y));
+    }
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? FVB_OK : cuda_fail(e, "csr matvec launch");
 }

@@ -291,3 +291,36 @@ def test_special_values_vs_reference(orc, ref, prec, dim):
                          (orc.jacobian(dim, s)[0], ref.jacobian(dim, s)[0])]:
         assert all(nan_aware_equal(x, y) for x, y in zip(mine, theirs))
     assert np.isnan(orc.wave_speed_max(dim, s)) and np.isnan(ref.jacobian(dim, s)[1])
+
+
+# ---- CSR block matvec ------------------------------------------------
+
+
+def random_csr(rng, rows, cols, max_row, empty_every=0):
+    """Sorted, duplicate-free rows (as SparseMatrix stores them), some empty."""
+    rp, ci, v = [0], [], []
+    for r in range(rows):
+        k = 0 if empty_every and r % empty_every == 0 else int(rng.integers(0, max_row + 1))
+        c = np.sort(rng.choice(cols, min(k, cols), replace=False))
+        ci += list(c)
+        v += list(rng.uniform(-2.0, 2.0, len(c)))
+        rp.append(len(ci))
+    return (np.array(rp, np.uint64), np.array(ci, np.uint64), np.array(v, np.float64))
+
+
+@pytest.mark.parametrize("y_prec", ["f64", "f32"])
+@pytest.mark.parametrize("x_prec", ["f64", "f32"])
+@pytest.mark.parametrize("m_prec", ["f64", "f32"])
+def test_csr_matvec_matches_reference(orc, ref, y_prec, x_prec, m_prec):
+    # The oracle's csr_matvec_acc restatement equals the reference's
+    # block_matvec + evaluate_block bit for bit (block.cpp:345-356, 428-446):
+    # short and long rows, empty rows, every precision combination.
+    rng = np.random.default_rng(7)
+    for rows, cols, max_row, empty in [(1, 1, 1, 0), (64, 50, 12, 5), (300, 1000, 200, 7),
+                                       (2000, 2000, 7, 0)]:
+        rp, ci, v = random_csr(rng, rows, cols, max_row, empty)
+        x = rng.uniform(-2.0, 2.0, cols).astype(np.float64 if x_prec == "f64" else np.float32)
+        want, stored = ref.csr_matvec(rp, ci, v, x, cols, y_prec=y_prec, m_prec=m_prec)
+        y0 = np.zeros(rows, np.float64 if y_prec == "f64" else np.float32)
+        got = orc.csr_matvec_acc(rp, ci, stored, x, y0)
+        assert got.tobytes() == want.tobytes(), (rows, cols)

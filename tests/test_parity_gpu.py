@@ -565,3 +565,54 @@ def test_beyond_32bit_indices(cuda, orc):
         assert np.float32(orc.wave_speed_max(dim, pt)).tobytes() == got_lam[k].tobytes(), int(i)
     del s, lam_pts
     torch.cuda.empty_cache()
+
+
+# ---- CSR block matvec ------------------------------------------------
+
+
+def _csr_to_dev(rp, ci, v, cuda):
+    return (torch.from_numpy(rp.view(np.int64)).to(cuda),
+            torch.from_numpy(ci.view(np.int64)).to(cuda), torch.from_numpy(v).to(cuda))
+
+
+def stencil7(n):
+    """7-point Laplacian on an n^3 grid, rows column-sorted (as stored)."""
+    rows = n ** 3
+    r = np.arange(rows, dtype=np.int64)
+    i, j, k = r % n, (r // n) % n, r // (n * n)
+    offs = [-(n * n), -n, -1, 0, 1, n, n * n]
+    ok = [k > 0, j > 0, i > 0, np.ones(rows, bool), i + 1 < n, j + 1 < n, k + 1 < n]
+    cols = np.stack([r + o for o in offs], 1)
+    mask = np.stack(ok, 1)
+    vals = np.where(np.arange(7) == 3, 6.0, -1.0)[None, :].repeat(rows, 0)
+    counts = mask.sum(1)
+    rp = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64)
+    return rp, cols[mask].astype(np.uint64), vals[mask].astype(np.float64)
+
+
+@pytest.mark.parametrize("y_prec,x_prec", [("f64", "f64"), ("f64", "f32"), ("f32", "f64"),
+                                           ("f32", "f32")])
+def test_csr_matvec_bitwise(cuda, orc, y_prec, x_prec):
+    # The warp-staged kernel against the oracle (pinned to the reference in
+    # test_oracle.py): rows longer than one staging tile, warps whose range
+    # spans several tiles, empty rows, a ragged last warp, a 7-point
+    # stencil -- and the accumulation into a nonzero y.
+    from tests.test_oracle import random_csr
+    rng = np.random.default_rng(11)
+    yt = {"f64": np.float64, "f32": np.float32}
+    cases = [random_csr(rng, 1, 1, 1), random_csr(rng, 37, 3000, 1000, 3),
+             random_csr(rng, 4099, 5000, 40, 9), stencil7(48)]
+    for rp, ci, v in cases:
+        rows = len(rp) - 1
+        cols = int(ci.max()) + 1 if len(ci) else 1
+        x = rng.uniform(-2, 2, cols).astype(yt[x_prec])
+        y0 = rng.uniform(-1, 1, rows).astype(yt[y_prec])
+        want = orc.csr_matvec_acc(rp, ci, v, x, y0)
+        drp, dci, dv = _csr_to_dev(rp, ci, v, cuda)
+        dx = torch.from_numpy(x).to(cuda)
+        dy = torch.from_numpy(y0.copy()).to(cuda)
+        N.check(N.lib().fvb_csr_matvec_acc(PREC[y_prec], PREC[x_prec], rows, len(ci),
+                                           drp.data_ptr(), dci.data_ptr(), dv.data_ptr(),
+                                           dx.data_ptr(), dy.data_ptr(),
+                                           torch.cuda.current_stream().cuda_stream))
+        assert same_bits(to_host([dy])[0], want), rows
