@@ -49,8 +49,8 @@ __global__ void __launch_bounds__(kCsrThreads)
 }
 
 // Warp-staged: see the file comment.  One warp per 32 rows, grid-stride.
-template <class TY, class TX>
-__global__ void __launch_bounds__(kCsrThreads)
+template <class TY, class TX, int MINB, int UNR>
+__global__ void __launch_bounds__(kCsrThreads, MINB)
     csr_warp_kernel(uint64_t rows, const uint64_t* __restrict__ rp,
                     const uint64_t* __restrict__ ci, const double* __restrict__ v,
                     const TX* __restrict__ x, TY* __restrict__ y) {
@@ -68,14 +68,17 @@ __global__ void __launch_bounds__(kCsrThreads)
         const uint64_t E = __shfl_sync(0xffffffffu, end, unsigned(last));
         TY acc = 0;
         for (uint64_t base = B; base < E; base += kTile) {
-            const uint64_t lim = E - base < uint64_t(kTile) ? E - base : uint64_t(kTile);
-#pragma unroll 4
-            for (uint64_t t = lane; t < lim; t += 32)
-                p[t] = static_cast<TY>(v[base + t]) * static_cast<TY>(x[ci[base + t]]);
+            const unsigned lim = E - base < uint64_t(kTile) ? unsigned(E - base) : unsigned(kTile);
+            const double* vb = v + base;
+            const uint64_t* cb = ci + base;
+#pragma unroll UNR
+            for (unsigned t = lane; t < lim; t += 32)
+                p[t] = static_cast<TY>(vb[t]) * static_cast<TY>(x[cb[t]]);
             __syncwarp();
-            const uint64_t lo = beg > base ? beg : base;
-            const uint64_t hi = end < base + lim ? end : base + lim;
-            for (uint64_t k = lo; k < hi; ++k) acc = acc + p[k - base];
+            // this lane's row within the tile: [clamp(beg-base), clamp(end-base))
+            const unsigned lo = beg <= base ? 0u : (beg - base < lim ? unsigned(beg - base) : lim);
+            const unsigned hi = end <= base ? 0u : (end - base < lim ? unsigned(end - base) : lim);
+            for (unsigned k = lo; k < hi; ++k) acc = acc + p[k];
             __syncwarp();
         }
         if (valid) y[r] = y[r] + acc;
@@ -102,8 +105,12 @@ fvb_status launch_csr(uint64_t rows, const uint64_t* rp, const uint64_t* ci, con
         uint64_t grid = (warps + kCsrThreads / 32 - 1) / (kCsrThreads / 32);
         const uint64_t cap = uint64_t(device_sm_count()) * 8 * 64;
         grid = grid < cap ? grid : cap;
-        csr_warp_kernel<TY, TX><<<unsigned(grid ? grid : 1), kCsrThreads, 0, s>>>(
-            rows, rp, ci, v, static_cast<const TX*>(x), static_cast<TY*>(y));
+        const unsigned g = unsigned(grid ? grid : 1);
+        const TX* xx = static_cast<const TX*>(x);
+        TY* yy = static_cast<TY*>(y);
+        // 8 resident CTAs (32 registers) and two tile entries in flight per
+        // lane: the measured best (profiles/r01_csr_shapes.txt)
+        csr_warp_kernel<TY, TX, 8, 2><<<g, kCsrThreads, 0, s>>>(rows, rp, ci, v, xx, yy);
     }
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? FVB_OK : cuda_fail(e, "csr matvec launch");

@@ -85,7 +85,7 @@ def main():
             "bitwise_vs_oracle": bitwise, "l2": "flushed between reps"}
     print(json.dumps(line), flush=True)
     ref = oracle.reference()
-    if ref is not None and variant == "warp":
+    if ref is not None and variant == "warp" and a.ref_n > 0:
         ts, rnnz = ref.time_csr(a.ref_n, 5)
         rrows = a.ref_n ** 3
         print(json.dumps({"kernel": "reference csr_matvec_acc (serial, 1 core)",
