@@ -477,6 +477,14 @@ void run_matvec(const DeviceBackend& be, std::vector<std::pair<const BlockItem*,
             if (x.size() != t.mat->cols())
                 throw LengthMismatch("matvec column count " + std::to_string(t.mat->cols()) +
                                      " vs operand length " + std::to_string(x.size()));
+            const int py = y->precision() == Precision::f64 ? 1 : 0;
+            const int px = x.precision() == Precision::f64 ? 1 : 0;
+            if (const DeviceCsr* dm = be.residency ? be.residency->find(t.mat) : nullptr) {
+                // a resident matrix: no upload
+                fvb_check(fvb_csr_matvec_acc(py, px, rows, dm->nnz(), dm->row_ptr(),
+                                             dm->col_idx(), dm->values(), x.data(), y->data(), s));
+                continue;
+            }
             const auto& rp = t.mat->row_ptr();
             const auto& ci = t.mat->col_idx();
             const auto& v = t.mat->values();
@@ -488,13 +496,13 @@ void run_matvec(const DeviceBackend& be, std::vector<std::pair<const BlockItem*,
                 cuda_check(cudaMemcpyAsync(dci.p, ci.data(), ci.size() * 8, cudaMemcpyHostToDevice, s), "csr upload");
                 cuda_check(cudaMemcpyAsync(dv.p, v.data(), v.size() * 8, cudaMemcpyHostToDevice, s), "csr upload");
             }
-            fvb_check(fvb_csr_matvec_acc(y->precision() == Precision::f64 ? 1 : 0,
-                                         x.precision() == Precision::f64 ? 1 : 0, rows, ci.size(),
+            fvb_check(fvb_csr_matvec_acc(py, px, rows, ci.size(),
                                          static_cast<const uint64_t*>(drp.p),
                                          static_cast<const uint64_t*>(dci.p),
                                          static_cast<const double*>(dv.p), x.data(), y->data(), s));
             cuda_check(cudaStreamSynchronize(s), "matvec");  // before the CSR buffers go
         }
+        cuda_check(cudaStreamSynchronize(s), "matvec");
         if (d.host && rows)
             cuda_check(cudaMemcpy(d.host->raw(), y->data(), y->byte_size(), cudaMemcpyDeviceToHost),
                        "matvec read-back");
@@ -738,6 +746,55 @@ void Residency::unbind(const DenseVector& host) { map_.erase(&host); }
 DeviceVector* Residency::find(const DenseVector* host) const {
     auto it = map_.find(host);
     return it == map_.end() ? nullptr : it->second;
+}
+
+void Residency::bind(const SparseMatrix& host, DeviceCsr& dev) {
+    if (host.rows() != dev.rows() || host.cols() != dev.cols() || host.nnz() != dev.nnz())
+        throw ShapeMismatch("bind: the device CSR copy has another shape");
+    csr_[&host] = &dev;
+}
+
+void Residency::unbind(const SparseMatrix& host) { csr_.erase(&host); }
+
+DeviceCsr* Residency::find(const SparseMatrix* host) const {
+    auto it = csr_.find(host);
+    return it == csr_.end() ? nullptr : it->second;
+}
+
+DeviceCsr::DeviceCsr(const SparseMatrix& m, int ordinal) : ordinal_(ordinal) { upload(m); }
+
+DeviceCsr::~DeviceCsr() {
+    if (rp_) cudaFree(rp_);
+    if (ci_) cudaFree(ci_);
+    if (v_) cudaFree(v_);
+}
+
+void DeviceCsr::upload(const SparseMatrix& m) {
+    static_assert(sizeof(std::size_t) == sizeof(std::uint64_t), "64-bit size_t");
+    DeviceGuard guard(ordinal_);
+    if (m.rows() != rows_ || m.nnz() != nnz_ || !rp_) {
+        if (rp_) cudaFree(rp_);
+        if (ci_) cudaFree(ci_);
+        if (v_) cudaFree(v_);
+        rp_ = ci_ = nullptr;
+        v_ = nullptr;
+        cuda_check(cudaMalloc(&rp_, (m.rows() + 1) * 8), "csr allocation");
+        if (m.nnz()) {
+            cuda_check(cudaMalloc(&ci_, m.nnz() * 8), "csr allocation");
+            cuda_check(cudaMalloc(&v_, m.nnz() * 8), "csr allocation");
+        }
+    }
+    rows_ = m.rows();
+    cols_ = m.cols();
+    nnz_ = m.nnz();
+    cuda_check(cudaMemcpy(rp_, m.row_ptr().data(), (rows_ + 1) * 8, cudaMemcpyHostToDevice),
+               "csr upload");
+    if (nnz_) {
+        cuda_check(cudaMemcpy(ci_, m.col_idx().data(), nnz_ * 8, cudaMemcpyHostToDevice),
+                   "csr upload");
+        cuda_check(cudaMemcpy(v_, m.values().data(), nnz_ * 8, cudaMemcpyHostToDevice),
+                   "csr upload");
+    }
 }
 
 // ---- keys ---------------------------------------------------------------------

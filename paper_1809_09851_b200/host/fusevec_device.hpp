@@ -89,14 +89,46 @@ DeviceVector make_temp(Precision prec, std::size_t len);
 
 /// Binds host DenseVector leaves to device-resident copies: expressions
 /// whose leaves are bound read the device planes and move no host memory.
+/// A SparseMatrix's CSR arrays uploaded once (row pointers, column indices
+/// and the stored values, block.hpp:42-44), for repeated block matvecs
+/// without re-sending the matrix over PCIe.  A snapshot: re-upload after
+/// SparseMatrix::set_value.
+class DeviceCsr {
+  public:
+    explicit DeviceCsr(const SparseMatrix& m, int ordinal = 0);
+    ~DeviceCsr();
+    DeviceCsr(const DeviceCsr&) = delete;
+    DeviceCsr& operator=(const DeviceCsr&) = delete;
+
+    void upload(const SparseMatrix& m);  // refresh from the host matrix
+    std::size_t rows() const { return rows_; }
+    std::size_t cols() const { return cols_; }
+    std::size_t nnz() const { return nnz_; }
+    const std::uint64_t* row_ptr() const { return rp_; }
+    const std::uint64_t* col_idx() const { return ci_; }
+    const double* values() const { return v_; }
+
+  private:
+    int ordinal_ = 0;
+    std::size_t rows_ = 0, cols_ = 0, nnz_ = 0;
+    std::uint64_t* rp_ = nullptr;
+    std::uint64_t* ci_ = nullptr;
+    double* v_ = nullptr;
+};
+
 class Residency {
   public:
     void bind(const DenseVector& host, DeviceVector& dev);
     void unbind(const DenseVector& host);
     DeviceVector* find(const DenseVector* host) const;
+    /// Block matvecs with this matrix read the device copy.
+    void bind(const SparseMatrix& host, DeviceCsr& dev);
+    void unbind(const SparseMatrix& host);
+    DeviceCsr* find(const SparseMatrix* host) const;
 
   private:
     std::unordered_map<const DenseVector*, DeviceVector*> map_;
+    std::unordered_map<const SparseMatrix*, DeviceCsr*> csr_;
 };
 
 /// Evaluation strategy for the device path (the analog of Backend).

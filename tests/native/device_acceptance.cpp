@@ -419,7 +419,25 @@ void run_gpu() {
         evaluate_block(ref, p32, w3);
         dev::evaluate_block(be, p32, g3);
         if (!same_bits(w3.get(0), g3.get(0))) fail("mixed-precision matvec differs");
-        return std::to_string(cases) + " random block shapes bitwise; identity case all ones";
+        // a device-resident matrix (DeviceCsr bound in a Residency): same bits,
+        // and a refreshed copy follows SparseMatrix::set_value
+        dev::DeviceCsr da(a, be.ordinal);
+        dev::Residency res;
+        res.bind(a, da);
+        dev::DeviceBackend rb = be;
+        rb.residency = &res;
+        std::vector<DenseVector> r32;
+        r32.emplace_back(Precision::f32, 4);
+        BlockColVector gr(std::move(r32));
+        dev::evaluate_block(rb, p32, gr);
+        if (!same_bits(w3.get(0), gr.get(0))) fail("resident-matrix matvec differs");
+        a.set_value(2, 1, 0.25);
+        da.upload(a);
+        evaluate_block(ref, p32, w3);
+        dev::evaluate_block(rb, p32, gr);
+        if (!same_bits(w3.get(0), gr.get(0))) fail("refreshed resident matrix differs");
+        return std::to_string(cases) +
+               " random block shapes bitwise; identity case all ones; resident matrix";
     });
 
     check("criterion 6 on device: flux, d in {1,2,3} x 100 instances, n=64, bitwise", [&] {
