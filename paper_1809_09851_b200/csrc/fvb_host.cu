@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -145,7 +146,11 @@ struct DeviceGuard {
     }
 };
 
-fvb_status ensure_buffers(fvb_ctx* ctx, size_t dev_bytes, size_t pin_bytes) {
+// Device staging (required) and pinned bounce buffers (optional: *pinned is
+// false when the host has no pinned memory to give; the caller then copies
+// pageable planes with plain cudaMemcpyAsync, slower but correct).
+fvb_status ensure_buffers(fvb_ctx* ctx, size_t dev_bytes, size_t pin_bytes, bool* pinned) {
+    *pinned = true;
     if (dev_bytes > ctx->slot_bytes || pin_bytes > ctx->pin_bytes) {
         for (int s = 0; s < fvb_ctx::kSlots; ++s) cudaStreamSynchronize(ctx->stream[s]);
     }
@@ -168,8 +173,15 @@ fvb_status ensure_buffers(fvb_ctx* ctx, size_t dev_bytes, size_t pin_bytes) {
         }
         ctx->pin_bytes = 0;
         for (int s = 0; s < fvb_ctx::kSlots; ++s) {
-            const cudaError_t e = cudaHostAlloc(&ctx->pin_buf[s], pin_bytes, cudaHostAllocDefault);
-            if (e != cudaSuccess) return cuda_fail(e, "pinned bounce allocation");
+            if (cudaHostAlloc(&ctx->pin_buf[s], pin_bytes, cudaHostAllocDefault) != cudaSuccess) {
+                cudaGetLastError();  // not sticky: fall back to unbounced copies
+                for (int q = 0; q <= s; ++q) {
+                    if (ctx->pin_buf[q]) cudaFreeHost(ctx->pin_buf[q]);
+                    ctx->pin_buf[q] = nullptr;
+                }
+                *pinned = false;
+                return FVB_OK;
+            }
         }
         ctx->pin_bytes = pin_bytes;
     }
@@ -261,9 +273,23 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
                 any_pageable = true;
             }
         }
+    // FVB_HOST_BOUNCE=0 disables the bounce buffers (tests of the fallback)
+    static const bool allow_bounce = [] {
+        const char* e = std::getenv("FVB_HOST_BOUNCE");
+        return !(e && e[0] == '0' && e[1] == '\0');
+    }();
+    if (!allow_bounce) pin_bpp = 0;
     const uint64_t chunk = chunk_for(ctx, std::max<size_t>(dev_bpp, 1), n);
-    if (fvb_status st = ensure_buffers(ctx, size_t(chunk) * dev_bpp, size_t(chunk) * pin_bpp))
+    bool bounce = allow_bounce;
+    bool got_pinned = true;
+    if (fvb_status st =
+            ensure_buffers(ctx, size_t(chunk) * dev_bpp, size_t(chunk) * pin_bpp, &got_pinned))
         return st;
+    bounce = bounce && got_pinned;
+    if (!bounce) {  // no pinned memory: pageable planes go through cudaMemcpyAsync as they are
+        for (Arg& a : args) a.has_pin = false;
+        any_pageable = false;
+    }
     if (any_pageable && !ctx->pool) {
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         ctx->pool.reset(new (std::nothrow) CopyPool(std::min(16u, hw) - 1));

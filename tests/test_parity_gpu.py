@@ -616,3 +616,26 @@ def test_csr_matvec_bitwise(cuda, orc, y_prec, x_prec):
                                            dx.data_ptr(), dy.data_ptr(),
                                            torch.cuda.current_stream().cuda_stream))
         assert same_bits(to_host([dy])[0], want), rows
+
+
+def test_host_path_without_bounce_buffers(cuda):
+    # With no pinned memory to spare (forced here by FVB_HOST_BOUNCE=0) the
+    # pageable host path falls back to plain cudaMemcpyAsync: still bitwise.
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, oracle, paper_1809_09851_b200 as fvb
+orc = oracle.oracle()
+s = orc.random_state(3, 300_001, seed=17)
+ctx = fvb.HostContext(0, chunk_points=1 << 16)
+out = [torch.empty(300_001, dtype=torch.float64) for _ in range(15)]
+ctx.flux([torch.from_numpy(a) for a in s], 3, out)
+want = orc.flux(3, s)
+assert all(o.numpy().tobytes() == w.tobytes() for o, w in zip(out, want))
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FVB_HOST_BOUNCE="0")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
