@@ -304,6 +304,81 @@ struct HostCopies {
     }
 };
 
+// The CFL maximum of several slices, combined the way the kernel combines
+// points: IEEE bit patterns of the kernel's precision compared as unsigned
+// integers (wave speeds are >= 0; a NaN anywhere wins).
+double combine_max(const std::vector<double>& v, bool f64) {
+    uint64_t best = 0;
+    for (double x : v) {
+        uint64_t b;
+        if (f64) {
+            std::memcpy(&b, &x, 8);
+        } else {
+            const float f = static_cast<float>(x);
+            uint32_t u;
+            std::memcpy(&u, &f, 4);
+            b = u;
+        }
+        best = b > best ? b : best;
+    }
+    if (f64) {
+        double d;
+        std::memcpy(&d, &best, 8);
+        return d;
+    }
+    const uint32_t u = static_cast<uint32_t>(best);
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+// A host-buffer evaluation spread over DeviceBackend::ordinals: slice g of
+// [0, n) runs on ordinal g through that device's host context, all slices at
+// once on their own host threads (each device has its own PCIe link).
+double run_sliced(const DeviceBackend& be, const Plan& plan, std::size_t n,
+                  const std::vector<void*>& args, const std::vector<uint8_t>& prec,
+                  const std::vector<uint8_t>& on_dev, bool reduce,
+                  const std::vector<std::pair<DenseVector*, const DenseVector*>>& pass) {
+    const std::size_t G = be.ordinals.size();
+    std::vector<double> lam(G, 0.0);
+    std::vector<fvb_status> st(G, FVB_OK);
+    std::vector<std::string> err(G);
+    {
+        HostCopies copies(pass);
+        std::vector<std::thread> pool;
+        for (std::size_t g = 0; g < G; ++g) {
+            const std::size_t lo = n * g / G, hi = n * (g + 1) / G;
+            if (hi == lo) continue;
+            pool.emplace_back([&, g, lo, hi] {
+                std::vector<void*> a(args);
+                for (std::size_t i = 0; i < a.size(); ++i)
+                    if (a[i] && on_dev[i] == 0) a[i] = static_cast<char*>(a[i]) + lo * (prec[i] ? 8 : 4);
+                HostCtx& hc = host_ctx(be.ordinals[g]);
+                std::lock_guard<std::mutex> lock(hc.mu);
+                fvb_status s = FVB_OK;
+                if (!hc.ctx) s = fvb_ctx_create(be.ordinals[g], be.chunk_points, &hc.ctx);
+                if (s == FVB_OK)
+                    s = fvb_launch_host(hc.ctx, &plan.k, hi - lo, a.data(), prec.data(),
+                                        on_dev.data(), reduce ? &lam[g] : nullptr, nullptr);
+                st[g] = s;
+                if (s != FVB_OK) err[g] = fvb_last_error();
+            });
+        }
+        for (auto& t : pool) t.join();
+    }
+    for (std::size_t g = 0; g < G; ++g)
+        if (st[g] != FVB_OK) {
+            const std::string msg = "device " + std::to_string(be.ordinals[g]) + ": " + err[g];
+            switch (st[g]) {
+                case FVB_ELEN: throw LengthMismatch(msg);
+                case FVB_EUNSUPPORTED: throw UnsupportedExpression(msg);
+                case FVB_ECUDA: throw DeviceError(msg);
+                default: throw Error(msg);
+            }
+        }
+    return reduce ? combine_max(lam, plan.k.prec != 0) : 0.0;
+}
+
 // Execute a plan over [0, n).  Device planes (resident leaves, device
 // destinations) are used in place; with every plane on the device it is one
 // launch on the backend's stream.  Otherwise fvb_launch_host streams the
@@ -356,17 +431,23 @@ void run(const DeviceBackend& be, Plan& plan, std::size_t n, void* red) {
         cuda_check(cudaStreamSynchronize(s), "sync");
         return;
     }
-    HostCtx& hc = host_ctx(be.ordinal);
-    std::lock_guard<std::mutex> lock(hc.mu);
-    if (!hc.ctx) fvb_check(fvb_ctx_create(be.ordinal, be.chunk_points, &hc.ctx));
+    bool all_host = true;
+    for (uint8_t d : on_dev) all_host = all_host && d != 1;
     double lam = 0.0;
-    fvb_status st;
-    {
-        HostCopies copies(pass);  // joined before the result is returned
-        st = fvb_launch_host(hc.ctx, &plan.k, n, args.data(), prec.data(), on_dev.data(),
-                             red ? &lam : nullptr, be.stream);
+    if (be.ordinals.size() > 1 && all_host) {
+        lam = run_sliced(be, plan, n, args, prec, on_dev, red != nullptr, pass);
+    } else {
+        HostCtx& hc = host_ctx(be.ordinal);
+        std::lock_guard<std::mutex> lock(hc.mu);
+        if (!hc.ctx) fvb_check(fvb_ctx_create(be.ordinal, be.chunk_points, &hc.ctx));
+        fvb_status st;
+        {
+            HostCopies copies(pass);  // joined before the result is returned
+            st = fvb_launch_host(hc.ctx, &plan.k, n, args.data(), prec.data(), on_dev.data(),
+                                 red ? &lam : nullptr, be.stream);
+        }
+        fvb_check(st);
     }
-    fvb_check(st);
     if (red) {  // hand the maximum back through the caller's device scalar
         if (plan.k.prec) {
             cuda_check(cudaMemcpy(red, &lam, sizeof lam, cudaMemcpyHostToDevice), "lambda");

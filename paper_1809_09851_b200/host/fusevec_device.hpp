@@ -137,6 +137,11 @@ struct DeviceBackend {
     void* stream = nullptr;              // cudaStream_t; nullptr = legacy default
     const Residency* residency = nullptr;
     std::size_t chunk_points = 0;  // host-buffer staging chunk (0 = 256 MiB of device staging per slot)
+    /// Host-buffer evaluations (every plane a host vector) may spread over
+    /// several devices: the range is cut into one contiguous slice per
+    /// ordinal, each streamed over its own PCIe link in parallel, and the CFL
+    /// maxima combined exactly.  Empty = `ordinal` alone.
+    std::vector<int> ordinals;
 };
 
 /// UETLI tie: a list of device destinations a multi-output block writes in

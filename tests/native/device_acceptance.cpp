@@ -25,6 +25,8 @@
 #include <thread>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "fusevec/block.hpp"
 #include "fusevec/fluid.hpp"
 #include "fusevec/rng.hpp"
@@ -575,6 +577,48 @@ void run_gpu() {
             if (dev::reduce_max(be, wave_speed(u)) != m) fail("reduce_max differs");
         }
         return "";
+    });
+
+    check("host vectors over several devices (DeviceBackend::ordinals), flux + CFL", [&] {
+        // Each ordinal streams its own slice; on this one-GPU box the same
+        // device serves every slice, which exercises the slicing, the
+        // per-slice pointer offsets and the exact max-combine.
+        int devices = 0;
+        cudaGetDeviceCount(&devices);
+        for (std::size_t G : {2u, 3u}) {
+            dev::DeviceBackend mb = be;
+            for (std::size_t g = 0; g < G; ++g) mb.ordinals.push_back(int(g) % devices);
+            SplitMix64 rng(40 + G);
+            const std::size_t n = 100003;
+            auto f = random_state(3, n, rng);
+            StateSet u = state_conservative(EosSpec(), 3, leaves_of(f));
+            BlockVectorGrid want(5, 3, Precision::f64, n), got(5, 3, Precision::f64, n);
+            evaluate_block(ref, inviscid_flux(u), want);
+            dev::evaluate_block(mb, inviscid_flux(u), got);
+            for (std::size_t i = 0; i < 15; ++i)
+                if (!same_bits(want.get(i), got.get(i))) fail("flux item " + std::to_string(i));
+            const std::size_t m = 20011;
+            auto g3 = random_state(3, m, rng, Precision::f32);
+            StateSet w = state_conservative(EosSpec(), 3, leaves_of(g3));
+            BlockExpr J = inviscid_flux_jacobian(w);
+            BlockVectorGrid jw(15, 5, Precision::f32, m), jg(15, 5, Precision::f32, m);
+            evaluate_block(ref, J, jw);
+            // (the fused CFL reduction is a hand-written kernel: under
+            // FVB_FORCE_LOWER the block runs lowered, without it)
+            const bool lowered = std::getenv("FVB_FORCE_LOWER") != nullptr;
+            const double lam = lowered ? 0.0 : dev::evaluate_block_cfl(mb, J, jg);
+            if (lowered) dev::evaluate_block(mb, J, jg);
+            for (std::size_t i = 0; i < 75; ++i)
+                if (!same_bits(jw.get(i), jg.get(i))) fail("jacobian item " + std::to_string(i));
+            if (lowered) continue;
+            DenseVector ws(Precision::f32, m);
+            evaluate(ref, wave_speed(w), ws);
+            double mx = 0;
+            for (std::size_t i = 0; i < m; ++i) mx = std::fmax(mx, ws.at(i));
+            if (lam != mx) fail("sliced CFL max differs");
+            if (dev::reduce_max(mb, wave_speed(w)) != mx) fail("sliced reduce_max differs");
+        }
+        return std::to_string(devices) + " visible device(s)";
     });
 
     check("device-resident leaves (Residency) and tie'd make_temp destinations", [&] {
