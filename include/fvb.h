@@ -236,9 +236,11 @@ struct fvb_kernel {
  * items, each node in its own precision with operands converted first and
  * constants as exact hex literals (the reference's emit / emit_as rules),
  * compiled by NVRTC for sm_100a with --fmad=false and cached per key for
- * the process lifetime.  FVB_EUNSUPPORTED for a malformed key, a
- * non-finite constant or when NVRTC is unavailable; FVB_ECUDA when the
- * compiled kernel cannot be loaded (no device). */
+ * the process lifetime (and the compiled image on disk under
+ * $FVB_CACHE_DIR, default ~/.cache/fvb, keyed by the exact source and NVRTC
+ * version; FVB_CACHE_DIR=off disables it).  FVB_EUNSUPPORTED for a
+ * malformed key, a non-finite constant or when NVRTC is unavailable;
+ * FVB_ECUDA when the compiled kernel cannot be loaded (no device). */
 FVB_API fvb_status fvb_lookup(const char* key, fvb_kernel* out);
 
 /* The CUDA source fvb_lookup would compile for `key` (NUL-terminated into
@@ -249,8 +251,10 @@ FVB_API fvb_status fvb_emit_source(const char* key, char* buf, size_t cap, size_
  * needed); *cubin_bytes receives the sm_100a image size. */
 FVB_API fvb_status fvb_nvrtc_compile(const char* key, size_t* cubin_bytes);
 
-/* Number of registered patterns and the i-th pattern (wildcards "C?*;"
- * stand for captured constants), for diagnostics and tests. */
+/* Number of registered patterns and the i-th pattern (a constant written
+ * "C<p>#<name>;" is a wildcard captured into consts under that name; every
+ * occurrence of one name must carry the same bits), for diagnostics and
+ * tests. */
 FVB_API uint32_t fvb_pattern_count(void);
 FVB_API const char* fvb_pattern(uint32_t i, const char** name);
 
