@@ -301,6 +301,14 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
             for (const Piece& q : p) std::memcpy(q.dst, q.src, q.bytes);
     };
 
+    // On every exit -- an error part-way included -- nothing this call
+    // enqueued may still be copying into or out of the caller's buffers.
+    struct Drain {
+        fvb_ctx* ctx;
+        ~Drain() {
+            for (int s = 0; s < fvb_ctx::kSlots; ++s) cudaStreamSynchronize(ctx->stream[s]);
+        }
+    } drain{ctx};
     const uint64_t nchunks = (n + chunk - 1) / chunk;
     int64_t pending[fvb_ctx::kSlots];
     for (auto& p : pending) p = -1;
