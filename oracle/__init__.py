@@ -85,6 +85,8 @@ class Oracle:
         L.fvo_wave_speed_f64.argtypes = [GasC, i32, u64, pp, vp]
         L.fvo_eos_p_f64.argtypes = [GasC, u64, vp, vp, vp]
         L.fvo_eos_T_f64.argtypes = [GasC, u64, vp, vp]
+        L.fvo_eos_p_f32.argtypes = [GasC, u64, vp, vp, vp]
+        L.fvo_eos_T_f32.argtypes = [GasC, u64, vp, vp]
         for yx in ("yd_xd", "yd_xs", "ys_xd", "ys_xs"):
             getattr(L, f"fvo_csr_matvec_acc_{yx}").argtypes = [u64, vp, vp, vp, vp, vp]
         self.L = L
@@ -173,8 +175,10 @@ class Oracle:
         p = np.empty_like(rho)
         T = np.empty_like(rho)
         g = gas or self.gas()
-        self.L.fvo_eos_p_f64(g, len(rho), rho.ctypes.data, e.ctypes.data, p.ctypes.data)
-        self.L.fvo_eos_T_f64(g, len(rho), e.ctypes.data, T.ctypes.data)
+        sfx = _prec_of(rho)
+        getattr(self.L, f"fvo_eos_p_{sfx}")(g, len(rho), rho.ctypes.data, e.ctypes.data,
+                                             p.ctypes.data)
+        getattr(self.L, f"fvo_eos_T_{sfx}")(g, len(rho), e.ctypes.data, T.ctypes.data)
         return p, T
 
 

@@ -64,6 +64,16 @@ void fvo_eos_T_f64(fvo_gas g, uint64_t n, const double* e, double* T) {
     for (uint64_t i = 0; i < n; ++i) T[i] = e[i] / g.cv;
 }
 
+void fvo_eos_p_f32(fvo_gas g, uint64_t n, const float* rho, const float* e, float* p) {
+    const float gm1 = (float)g.gm1;
+    for (uint64_t i = 0; i < n; ++i) p[i] = gm1 * (rho[i] * e[i]);
+}
+
+void fvo_eos_T_f32(fvo_gas g, uint64_t n, const float* e, float* T) {
+    const float cv = (float)g.cv;
+    for (uint64_t i = 0; i < n; ++i) T[i] = e[i] / cv;
+}
+
 void fvo_wave_speed_f64(fvo_gas g, int dim, uint64_t n, const double* const* in, double* out) {
     for (uint64_t i = 0; i < n; ++i) {
         double rho, m[3], rho_E;

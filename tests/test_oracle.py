@@ -324,3 +324,17 @@ def test_csr_matvec_matches_reference(orc, ref, y_prec, x_prec, m_prec):
         y0 = np.zeros(rows, np.float64 if y_prec == "f64" else np.float32)
         got = orc.csr_matvec_acc(rp, ci, stored, x, y0)
         assert got.tobytes() == want.tobytes(), (rows, cols)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_eos_matches_reference(orc, ref, prec):
+    # eos_ideal_p / eos_ideal_T (fluid.cpp:57-65) in both precisions, the
+    # default and a monatomic gas, bit for bit against the reference build
+    dt = np.float64 if prec == "f64" else np.float32
+    rng = np.random.default_rng(4)
+    rho = rng.uniform(0.1, 5.0, 10007).astype(dt)
+    e = rng.uniform(0.1, 9.0, 10007).astype(dt)
+    for cp, cv in [((7, 2), (5, 2)), ((5, 2), (3, 2))]:
+        want_p, want_T = ref.eos(rho, e, cp=cp, cv=cv)
+        got_p, got_T = orc.eos(rho, e, gas=orc.gas(cp, cv))
+        assert got_p.tobytes() == want_p.tobytes() and got_T.tobytes() == want_T.tobytes()

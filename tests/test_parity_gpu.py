@@ -639,3 +639,22 @@ print("ok")
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                          text=True, timeout=300)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_eos_bitwise(cuda, orc, prec):
+    # fvb_eos against the oracle (pinned to the reference in test_oracle.py),
+    # default and monatomic gas, ragged n; either output may be NULL
+    rng = np.random.default_rng(6)
+    for n in (1, 7, 4099, 1_000_003):
+        rho = rng.uniform(0.1, 5.0, n).astype(NP[prec])
+        e = rng.uniform(0.1, 9.0, n).astype(NP[prec])
+        for gas, g in [(None, orc.gas()), (fvb.Gas(5, 2, 3, 2), orc.gas((5, 2), (3, 2)))]:
+            p, T = fvb.eos(*to_dev([rho, e], cuda), gas=gas)
+            want_p, want_T = orc.eos(rho, e, gas=g)
+            assert all_same(to_host([p, T]), [want_p, want_T]), n
+    d_rho, d_e = to_dev([rho, e], cuda)
+    T_only = torch.empty_like(d_rho)
+    N.check(N.lib().fvb_eos(None, PREC[prec], n, d_rho.data_ptr(), d_e.data_ptr(), None,
+                            T_only.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    assert same_bits(to_host([T_only])[0], orc.eos(rho, e)[1])
