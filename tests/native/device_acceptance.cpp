@@ -579,6 +579,33 @@ void run_gpu() {
         return "";
     });
 
+    check("column-major blocks and destination grids map items logically", [&] {
+        // linear_index (block.hpp:14-18): a ColMajor grid stores item (r, c)
+        // at c*nrow + r; items are still matched by (r, c)
+        SplitMix64 rng(52);
+        const std::size_t n = 9001;
+        auto f = random_state(3, n, rng);
+        StateSet u = state_conservative(EosSpec(), 3, leaves_of(f));
+        BlockVectorGrid want(5, 3, Precision::f64, n, StorageOrder::ColMajor);
+        BlockVectorGrid got(5, 3, Precision::f64, n, StorageOrder::ColMajor);
+        evaluate_block(ref, inviscid_flux(u), want);
+        dev::evaluate_block(be, inviscid_flux(u), got);
+        for (std::size_t r = 0; r < 5; ++r)
+            for (std::size_t c = 0; c < 3; ++c)
+                if (!same_bits(want.item(r, c), got.item(r, c))) fail("flux into a ColMajor grid");
+        // a ColMajor block expression of mixed items into a RowMajor grid
+        DenseVector a = testutil::make_vec(Precision::f64, n, rng), b = testutil::make_vec(Precision::f64, n, rng);
+        std::vector<BlockItem> items{BlockItem(leaf(a) * leaf(b)), BlockItem(elem_sqrt(leaf(a))),
+                                     BlockItem(leaf(a) / leaf(b)), BlockItem(leaf(b) - leaf(a))};
+        BlockExpr e(2, 2, items, StorageOrder::ColMajor);
+        BlockVectorGrid w2(2, 2, Precision::f64, n), g2(2, 2, Precision::f64, n);
+        evaluate_block(ref, e, w2);
+        dev::evaluate_block(be, e, g2);
+        for (std::size_t i = 0; i < 4; ++i)
+            if (!same_bits(w2.get(i), g2.get(i))) fail("ColMajor block expression");
+        return "";
+    });
+
     check("host vectors over several devices (DeviceBackend::ordinals), flux + CFL", [&] {
         // Each ordinal streams its own slice; on this one-GPU box the same
         // device serves every slice, which exercises the slicing, the
