@@ -243,8 +243,13 @@ void run_gpu() {
         SplitMix64 rng(662);
         int exact = 0, approx = 0;
         std::size_t worst = 0;
-        for (int t = 0; t < 80; ++t) {
-            Expr e = gen.gen(rng, 4);
+        // FVB_ACC_TREES / FVB_ACC_DEPTH widen the sweep for stress runs
+        const char* nt = std::getenv("FVB_ACC_TREES");
+        const char* nd = std::getenv("FVB_ACC_DEPTH");
+        const int trees = nt && *nt ? std::atoi(nt) : 80;
+        const int depth = nd && *nd ? std::atoi(nd) : 4;
+        for (int t = 0; t < trees; ++t) {
+            Expr e = gen.gen(rng, depth);
             const Precision P = e.result_precision();
             DenseVector want(P, n), got(P, n);
             evaluate(ref, e, want);
