@@ -428,7 +428,7 @@ void run(const DeviceBackend& be, Plan& plan, std::size_t n, void* red) {
             fvb_check(plan.k.reduce(&plan.k, 0, n, args.data(), red, s));
         else
             fvb_check(plan.k.fn(&plan.k, 0, n, args.data(), s));
-        cuda_check(cudaStreamSynchronize(s), "sync");
+        if (be.synchronize || red) cuda_check(cudaStreamSynchronize(s), "sync");
         return;
     }
     bool all_host = true;
@@ -739,15 +739,25 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
         }
     }
     run(be, plan, n, red);
+    // Pass-through items: plain copies.  A device destination is filled in
+    // stream order on the backend's stream -- from the leaf's resident plane
+    // when it has one -- so asynchronous (and graph-captured) evaluations
+    // stay asynchronous.
+    cudaStream_t s = static_cast<cudaStream_t>(be.stream);
+    bool queued = false;
     for (auto& [src, d] : copies) {
         DeviceGuard guard(be.ordinal);
-        if (d.host)
+        if (d.host) {
             std::memcpy(d.host->raw(), src->raw(), d.host->byte_size());
-        else
-            cuda_check(cudaMemcpy(d.dev->data(), src->raw(), d.dev->byte_size(),
-                                  cudaMemcpyHostToDevice),
-                       "pass-through copy");
+            continue;
+        }
+        const DeviceVector* rs = be.residency ? be.residency->find(src) : nullptr;
+        cuda_check(cudaMemcpyAsync(d.dev->data(), rs ? rs->data() : src->raw(), d.dev->byte_size(),
+                                   rs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s),
+                   "pass-through copy");
+        queued = true;
     }
+    if (queued && be.synchronize) cuda_check(cudaStreamSynchronize(s), "pass-through copy");
 }
 
 double read_max(void* red, Precision p) {

@@ -142,6 +142,12 @@ struct DeviceBackend {
     /// ordinal, each streamed over its own PCIe link in parallel, and the CFL
     /// maxima combined exactly.  Empty = `ordinal` alone.
     std::vector<int> ordinals;
+    /// false: an evaluation whose planes are all on the device returns once
+    /// its kernel is enqueued on `stream` (no host wait), so a sequence of
+    /// evaluate / evaluate_block calls can overlap, or be captured into a
+    /// CUDA graph and replayed.  Calls that return a value (the CFL maxima)
+    /// and host-buffer evaluations always complete before returning.
+    bool synchronize = true;
 };
 
 /// UETLI tie: a list of device destinations a multi-output block writes in

@@ -611,6 +611,73 @@ void run_gpu() {
         return "";
     });
 
+    check("asynchronous evaluations captured into a CUDA graph (synchronize = false)", [&] {
+        // The reference's own calls -- evaluate_block of inviscid_flux and of
+        // convert(.., Primitive) -- on resident leaves into tie'd device
+        // planes, enqueued without host waits, captured once and replayed.
+        SplitMix64 rng(61);
+        const std::size_t n = 50001;
+        auto f = random_state(3, n, rng);
+        StateSet u = state_conservative(EosSpec(), 3, leaves_of(f));
+        std::vector<dev::DeviceVector> dv;
+        dev::Residency res;
+        for (auto& v : f) {
+            dv.emplace_back(v.precision(), v.size());
+            dv.back().upload(v);
+        }
+        for (std::size_t i = 0; i < f.size(); ++i) res.bind(f[i], dv[i]);
+        cudaStream_t s = nullptr;
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) fail("stream");
+        dev::DeviceBackend ab = be;
+        ab.residency = &res;
+        ab.stream = s;
+        ab.synchronize = false;
+        std::vector<dev::DeviceVector> fl, pr;
+        for (int i = 0; i < 15; ++i) fl.emplace_back(Precision::f64, n);
+        for (int i = 0; i < 5; ++i) pr.emplace_back(Precision::f64, n);
+        dev::Tie tf, tp;
+        for (auto& o : fl) tf.dests.push_back(&o);
+        for (auto& o : pr) tp.dests.push_back(&o);
+        BlockExpr flux = inviscid_flux(u);
+        BlockExpr prim = convert(u, Formulation::Primitive).block();
+        dev::evaluate_block(ab, flux, tf);  // warm: keys resolved outside the capture
+        dev::evaluate_block(ab, prim, tp);
+        cudaStreamSynchronize(s);
+        for (auto* v : {&fl, &pr})
+            for (auto& o : *v) cudaMemsetAsync(o.data(), 0, o.byte_size(), s);
+        cudaStreamSynchronize(s);
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+            fail("begin capture");
+        dev::evaluate_block(ab, flux, tf);
+        dev::evaluate_block(ab, prim, tp);
+        if (cudaStreamEndCapture(s, &g) != cudaSuccess) fail("end capture");
+        std::size_t nodes = 0;
+        cudaGraphGetNodes(g, nullptr, &nodes);
+        if (cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) fail("instantiate");
+        for (int rep = 0; rep < 3; ++rep) cudaGraphLaunch(ge, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess) fail("graph replay");
+        BlockVectorGrid want(5, 3, Precision::f64, n);
+        evaluate_block(ref, flux, want);
+        DenseVector tmp(Precision::f64, n);
+        for (std::size_t i = 0; i < 15; ++i) {
+            fl[i].download(tmp);
+            if (!same_bits(tmp, want.get(i))) fail("graph flux item " + std::to_string(i));
+        }
+        StateSet w = convert(u, Formulation::Primitive);
+        for (std::size_t i = 0; i < 5; ++i) {
+            DenseVector wi(Precision::f64, n);
+            evaluate(ref, w.field(i), wi);
+            pr[i].download(tmp);
+            if (!same_bits(tmp, wi)) fail("graph primitive field " + std::to_string(i));
+        }
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
+        cudaStreamDestroy(s);
+        return std::to_string(nodes) + " graph nodes";
+    });
+
     check("host vectors over several devices (DeviceBackend::ordinals), flux + CFL", [&] {
         // Each ordinal streams its own slice; on this one-GPU box the same
         // device serves every slice, which exercises the slicing, the
