@@ -299,7 +299,20 @@ def test_jacobian_cfl_1e8(cuda, orc):
         pt = orc.random_state(dim, 1, seed=0x5EED, first=int(i), prec="f32")
         want = np.array([a[0] for a in orc.jacobian(dim, pt)[0]], np.float32)
         assert same_bits(got[:, k], want), int(i)
-    del j, s, lam_pts
+    # size-independent property over all 1e8 points: Euler homogeneity,
+    # A_k(U) U = F_k(U), against the separately computed flux,
+    # accumulated in f64 from the f32 planes
+    f = fvb.flux(s, dim)
+    w = dim + 2
+    for kk in range(dim):
+        for r in range(w):
+            au = torch.zeros(n, dtype=torch.float64, device=cuda)
+            for c in range(w):
+                au += j[(kk * w + r) * w + c].double() * s[c].double()
+            fk = f[r * dim + kk].double()
+            err = (au - fk).abs() / torch.clamp(fk.abs(), min=1.0)
+            assert float(err.max()) < 1e-5, (kk, r, float(err.max()))
+    del j, s, lam_pts, f
     torch.cuda.empty_cache()
 
 
