@@ -264,6 +264,13 @@ fvb_status launch_op(const T* const* in, T* const* out, uint64_t n, const Consts
     // 16 warps of loads in flight, except for the 32- and 75-output Jacobians,
     // whose live state would spill under that cap.
     constexpr int MB = Op::NOUT > 24 ? 1 : 2;
+    // Small ranges (fewer 32-byte groups than one 256-thread CTA per SM):
+    // one element per thread in 64-thread CTAs, so even n = 1024 spreads
+    // over 16 SMs instead of running on one (launch-bound regime).
+    if (n < uint64_t(device_sm_count()) * 256 * VD) {
+        plan_range<T, 1>(ptrs, np, n, &rg);
+        return launch_fixed<Op, T, 1, 1, kStoreStreaming, RED, 64, MB>(pl, k, rg, red, stream);
+    }
     if (plan_range<T, VD>(ptrs, np, n, &rg))
         return launch_fixed<Op, T, VD, 1, kStoreStreaming, RED, 256, MB>(pl, k, rg, red, stream);
     // Planes with different 32-byte residues: element-wide accesses.
