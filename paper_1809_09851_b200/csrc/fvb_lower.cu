@@ -372,8 +372,13 @@ bool emit(const char* key, std::string* src, KDag* dag_out, bool wide = true, in
 
     s += "extern \"C\" __global__ void __launch_bounds__(" + T + ", " + num(minb) +
          ") fvb_gen(const FvbArgs a, const fvb_u64 n, const int vec)\n{\n";
-    // every plane 4-element aligned: 4 consecutive elements per thread with
-    // one wide access per plane; otherwise 4 elements strided by the CTA
+    // vec == 2 (small ranges): one element per thread, spread over many
+    // small CTAs; every plane 4-element aligned (vec == 1): 4 consecutive
+    // elements per thread with one wide access per plane; otherwise 4
+    // elements strided by the CTA
+    s += "    if (vec == 2) {\n";
+    s += "        const fvb_u64 i = (fvb_u64)blockIdx.x * blockDim.x + threadIdx.x;\n";
+    s += "        if (i < n) fvb_tile<1>(a, i);\n        return;\n    }\n";
     s += "    if (vec) {\n";
     s += "        const fvb_u64 i0 = ((fvb_u64)blockIdx.x * " + T + "ull + threadIdx.x) * 4ull;\n";
     s += "        if (i0 + 4ull <= n) {\n            fvb_tile<4>(a, i0);\n            return;\n"
@@ -647,13 +652,22 @@ fvb_status gen_entry(const fvb_kernel* k, uint64_t begin, uint64_t end, void* co
         const size_t w = g->arg_prec[i] == 's' ? sizeof(float) : sizeof(double);
         if (reinterpret_cast<uintptr_t>(la.p[i]) % (4 * w)) vec = 0;
     }
-    const uint64_t per = uint64_t(kThreads) * kPerThread;
+    // Small ranges (fewer elements than 4 per thread of one 256-thread CTA per
+    // SM): one element per thread in 64-thread CTAs, so n = 1024 runs on 16
+    // SMs instead of one (as launch_op does for the hand-written kernels).
+    unsigned threads = kThreads;
+    uint64_t per = uint64_t(kThreads) * kPerThread;
+    if (n < uint64_t(device_sm_count()) * kThreads * kPerThread) {
+        vec = 2;
+        threads = 64;
+        per = 64;
+    }
     const uint64_t grid = (n + per - 1) / per;
     if (grid > 0x7fffffffull) return fail(FVB_EARG, "range too large for one launch");
     void* params[] = {&la, &n, &vec};
     const cudaError_t e =
         cudaLaunchKernel(reinterpret_cast<const void*>(g->kernel), dim3(unsigned(grid)),
-                         dim3(kThreads), params, 0, static_cast<cudaStream_t>(stream));
+                         dim3(threads), params, 0, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? FVB_OK : cuda_fail(e, "lowered kernel launch");
 }
 
