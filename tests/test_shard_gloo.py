@@ -63,9 +63,12 @@ def _worker(rank, world, port, n_total, dim, result):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_total", [1, 10_001])
-def test_cfl_allreduce_max_gloo_world2(orc, n_total):
-    world, dim = 2, 3
+@pytest.mark.parametrize("world,n_total", [(2, 1), (2, 10_001), (3, 10_001), (8, 10_001),
+                                           (8, 5)])
+def test_cfl_allreduce_max_gloo(orc, world, n_total):
+    # ragged slices (N mod G != 0, and N < G: empty ranks) reduce to the
+    # single-process maximum bit for bit on every rank
+    dim = 3
     mgr = mp.Manager()
     result = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), n_total, dim, result), nprocs=world, join=True)
