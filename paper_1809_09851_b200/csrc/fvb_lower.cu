@@ -587,9 +587,18 @@ int env_int(const char* name, int dflt) {
 fvb_status build(const char* key, KDag* d, std::vector<char>* image, int* minb_out) {
     fvb_status last = FVB_EUNSUPPORTED;
     const int forced = env_int("FVB_LOWER_MINB", 0);  // tuning experiments only
+    // Blocks with many outputs keep more live state than the 2-CTA/SM
+    // register cap allows (the hand-written Jacobians spill under it too):
+    // they start without the cap, which saves a compile on first use.
+    std::string probe;
+    if (!emit(key, &probe, d, true, 2))
+        return fail(FVB_EUNSUPPORTED, std::string("not a loweable structural key: ") +
+                                          std::string(key).substr(0, 160));
+    const bool big = d && d->roots.size() > 24;
     for (bool wide : {true, false}) {
         for (int minb : {2, 1}) {
             if (forced && minb != forced) continue;
+            if (!forced && big && minb == 2) continue;
             std::string src;
             if (!emit(key, &src, d, wide, minb))
                 return fail(FVB_EUNSUPPORTED, std::string("not a loweable structural key: ") +
