@@ -15,6 +15,7 @@
 #include <memory>
 #include <mutex>
 #include <thread>
+#include <unordered_map>
 
 #include "fvb.h"
 
@@ -604,27 +605,37 @@ void leaves_of(const ExprNode& n, std::vector<const DenseVector*>& out) {
     }
 }
 
-// Does destination o name the storage leaf l reads?  A host destination is
-// the leaf itself; a device one is the leaf's resident copy.
-bool writes_leaf(const DeviceBackend& be, const Out& o, const DenseVector* l) {
-    if (o.host) return o.host == l;
-    return o.dev && be.residency && be.residency->find(l) == o.dev;
-}
-
 // True when some element-wise item reads a vector that an earlier item of
 // the block writes (or that a matvec row writes: those run first here).
 bool reads_earlier_destination(const DeviceBackend& be, const std::vector<Expr>& items,
                                const std::vector<Out>& outs,
                                const std::vector<std::pair<const BlockItem*, Out>>& matvecs) {
+    // The earliest item writing each destination (a host vector, or a device
+    // plane that is some leaf's resident copy); matvec rows count as written
+    // before every item.  Linear in the leaves, so a 75-item Jacobian block
+    // costs one pass over its trees.
+    std::unordered_map<const void*, long> writer;
+    for (const auto& mv : matvecs) {
+        const Out& o = mv.second;
+        if (o.host || o.dev) writer[o.host ? static_cast<const void*>(o.host) : o.dev] = -1;
+    }
+    for (std::size_t j = 0; j < outs.size(); ++j) {
+        const Out& o = outs[j];
+        if (o.host || o.dev)
+            writer.emplace(o.host ? static_cast<const void*>(o.host) : o.dev, long(j));
+    }
+    if (writer.empty()) return false;
     std::vector<const DenseVector*> ls;
     for (std::size_t k = 0; k < items.size(); ++k) {
         ls.clear();
         leaves_of(items[k].node(), ls);
         for (const DenseVector* l : ls) {
-            for (std::size_t j = 0; j < k; ++j)
-                if (writes_leaf(be, outs[j], l)) return true;
-            for (const auto& mv : matvecs)
-                if (writes_leaf(be, mv.second, l)) return true;
+            auto it = writer.find(l);
+            if (it != writer.end() && it->second < long(k)) return true;
+            if (const DeviceVector* dv = be.residency ? be.residency->find(l) : nullptr) {
+                it = writer.find(dv);
+                if (it != writer.end() && it->second < long(k)) return true;
+            }
         }
     }
     return false;
