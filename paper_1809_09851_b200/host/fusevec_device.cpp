@@ -135,13 +135,32 @@ struct Slots {
     }
 };
 
+// Small appenders for the key text (a 75-item Jacobian key is ~4 KB, built
+// on every evaluate_block call).
+void append_uint(std::string& out, std::size_t v) {
+    char buf[24];
+    int i = 0;
+    do {
+        buf[i++] = char('0' + v % 10);
+        v /= 10;
+    } while (v);
+    while (i) out += buf[--i];
+}
+
+void append_hex16(std::string& out, unsigned long long bits) {
+    static const char kHex[] = "0123456789abcdef";
+    char buf[16];
+    for (int i = 15; i >= 0; --i, bits >>= 4) buf[i] = kHex[bits & 15];
+    out.append(buf, 16);
+}
+
 // key_node (proj/src/backend_jit.cpp:112-155): same grammar, same order.
 void key_node(const ExprNode& n, Slots& slots, bool& ok, std::string& out) {
     switch (n.kind) {
         case NodeKind::Leaf:
             out += 'L';
             out += prec_char(n.prec);
-            out += std::to_string(slots.of(n.vec));
+            append_uint(out, slots.of(n.vec));
             out += ';';
             return;
         case NodeKind::Constant: {
@@ -149,9 +168,10 @@ void key_node(const ExprNode& n, Slots& slots, bool& ok, std::string& out) {
             if (!std::isfinite(v)) ok = false;
             unsigned long long bits;
             std::memcpy(&bits, &v, sizeof bits);
-            char buf[32];
-            std::snprintf(buf, sizeof buf, "C%c%016llx;", prec_char(n.prec), bits);
-            out += buf;
+            out += 'C';
+            out += prec_char(n.prec);
+            append_hex16(out, bits);
+            out += ';';
             return;
         }
         case NodeKind::Tagged:
@@ -160,7 +180,7 @@ void key_node(const ExprNode& n, Slots& slots, bool& ok, std::string& out) {
             return;
         case NodeKind::Unary:
             out += 'U';
-            out += std::to_string(static_cast<int>(n.uop));
+            append_uint(out, static_cast<std::size_t>(n.uop));
             out += prec_char(n.prec);
             out += '(';
             key_node(*n.left, slots, ok, out);
@@ -168,7 +188,7 @@ void key_node(const ExprNode& n, Slots& slots, bool& ok, std::string& out) {
             return;
         case NodeKind::Binary:
             out += 'B';
-            out += std::to_string(static_cast<int>(n.bop));
+            append_uint(out, static_cast<std::size_t>(n.bop));
             out += prec_char(n.prec);
             out += '(';
             key_node(*n.left, slots, ok, out);
@@ -429,7 +449,8 @@ void run(const DeviceBackend& be, Plan& plan, std::size_t n, void* red) {
             fvb_check(plan.k.reduce(&plan.k, 0, n, args.data(), red, s));
         else
             fvb_check(plan.k.fn(&plan.k, 0, n, args.data(), s));
-        if (be.synchronize || red) cuda_check(cudaStreamSynchronize(s), "sync");
+        // a reduction is read back (and waited for) by its caller, read_max
+        if (be.synchronize && !red) cuda_check(cudaStreamSynchronize(s), "sync");
         return;
     }
     bool all_host = true;
@@ -449,13 +470,12 @@ void run(const DeviceBackend& be, Plan& plan, std::size_t n, void* red) {
         }
         fvb_check(st);
     }
-    if (red) {  // hand the maximum back through the caller's device scalar
-        if (plan.k.prec) {
-            cuda_check(cudaMemcpy(red, &lam, sizeof lam, cudaMemcpyHostToDevice), "lambda");
-        } else {
-            const float f = static_cast<float>(lam);
-            cuda_check(cudaMemcpy(red, &f, sizeof f, cudaMemcpyHostToDevice), "lambda");
-        }
+    if (red) {  // hand the maximum back through the caller's device scalar, in stream order
+        const float f = static_cast<float>(lam);
+        cuda_check(cudaMemcpyAsync(red, plan.k.prec ? static_cast<const void*>(&lam) : &f,
+                                   plan.k.prec ? sizeof lam : sizeof f, cudaMemcpyHostToDevice, s),
+                   "lambda");
+        cuda_check(cudaStreamSynchronize(s), "lambda");
     }
 }
 
@@ -771,26 +791,45 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
     if (queued && be.synchronize) cuda_check(cudaStreamSynchronize(s), "pass-through copy");
 }
 
-double read_max(void* red, Precision p) {
-    if (p == Precision::f64) {
-        double v;
-        cuda_check(cudaMemcpy(&v, red, sizeof v, cudaMemcpyDeviceToHost), "lambda read-back");
-        return v;
-    }
-    float v;
-    cuda_check(cudaMemcpy(&v, red, sizeof v, cudaMemcpyDeviceToHost), "lambda read-back");
-    return double(v);
+// The maximum a reduction left in the device word, read back in stream
+// order on the backend's stream through a pinned word: one wait for the
+// kernel and the copy together.
+double read_max(const DeviceBackend& be, void* red, Precision p) {
+    struct Pinned {
+        void* p = nullptr;
+        ~Pinned() {
+            if (p) cudaFreeHost(p);
+        }
+    };
+    thread_local Pinned host;
+    if (!host.p) cuda_check(cudaHostAlloc(&host.p, 8, cudaHostAllocDefault), "pinned word");
+    cudaStream_t s = static_cast<cudaStream_t>(be.stream);
+    DeviceGuard guard(be.ordinal);
+    cuda_check(cudaMemcpyAsync(host.p, red, p == Precision::f64 ? 8 : 4, cudaMemcpyDeviceToHost, s),
+               "lambda read-back");
+    cuda_check(cudaStreamSynchronize(s), "lambda read-back");
+    if (p == Precision::f64) return *static_cast<const double*>(host.p);
+    return double(*static_cast<const float*>(host.p));
 }
 
+// The CFL accumulator: one 8-byte device word per host thread and device
+// (reused across calls), zeroed in stream order on the backend's stream
+// before each reduction.
 struct DeviceScalar {
     void* p = nullptr;
-    explicit DeviceScalar(int ordinal) {
-        DeviceGuard guard(ordinal);
-        cuda_check(cudaMalloc(&p, 8), "scalar allocation");
-        cuda_check(cudaMemset(p, 0, 8), "scalar reset");
-    }
-    ~DeviceScalar() {
-        if (p) cudaFree(p);
+    explicit DeviceScalar(const DeviceBackend& be) {
+        struct Cache {
+            std::map<int, void*> words;
+            ~Cache() {
+                for (auto& w : words) cudaFree(w.second);
+            }
+        };
+        thread_local Cache cache;
+        DeviceGuard guard(be.ordinal);
+        void*& word = cache.words[be.ordinal];
+        if (!word) cuda_check(cudaMalloc(&word, 8), "scalar allocation");
+        p = word;
+        cuda_check(cudaMemsetAsync(p, 0, 8, static_cast<cudaStream_t>(be.stream)), "scalar reset");
     }
 };
 
@@ -915,6 +954,7 @@ std::string block_key(const std::vector<Expr>& items, const std::vector<Precisio
     Slots slots;
     bool ok = true;
     std::string key = "G" + std::to_string(rows) + "x" + std::to_string(cols) + ":";
+    key.reserve(items.size() * 64);
     for (std::size_t i = 0; i < items.size(); ++i) {
         if (i) key += '|';
         key += prec_char(dests[i]);
@@ -1003,9 +1043,9 @@ double reduce_max(const DeviceBackend& be, const Expr& lambda) {
     none.null_prec = P;
     none.null_size = n;
     plan.outs = {none};
-    DeviceScalar red(be.ordinal);
+    DeviceScalar red(be);
     run(be, plan, n, red.p);
-    return read_max(red.p, P);
+    return read_max(be, red.p, P);
 }
 
 double evaluate_block_cfl(const DeviceBackend& be, const BlockExpr& jacobian,
@@ -1017,9 +1057,9 @@ double evaluate_block_cfl(const DeviceBackend& be, const BlockExpr& jacobian,
             o.host = &dest.item(r, c);
             outs.push_back(o);
         }
-    DeviceScalar red(be.ordinal);
+    DeviceScalar red(be);
     block_impl(be, jacobian, dest.block_rows(), dest.block_cols(), outs, red.p, true);
-    return read_max(red.p, dest.get(0).precision());
+    return read_max(be, red.p, dest.get(0).precision());
 }
 
 double evaluate_block_cfl(const DeviceBackend& be, const BlockExpr& jacobian, const Tie& dest) {
@@ -1029,9 +1069,9 @@ double evaluate_block_cfl(const DeviceBackend& be, const BlockExpr& jacobian, co
         o.dev = d;
         outs.push_back(o);
     }
-    DeviceScalar red(be.ordinal);
+    DeviceScalar red(be);
     block_impl(be, jacobian, jacobian.block_rows(), jacobian.block_cols(), outs, red.p, true);
-    return read_max(red.p, dest.dests.at(0)->precision());
+    return read_max(be, red.p, dest.dests.at(0)->precision());
 }
 
 }  // namespace device

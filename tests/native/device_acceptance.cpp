@@ -969,8 +969,79 @@ void run_perf(std::size_t n) {
                 "\"ms\": %.3f, \"gpts\": %.4f}\n", n, s * 1e3, n / s / 1e9);
 }
 
+// Host overhead of one reference-API call at small n: the adapter's key
+// building, lookup and launch, with resident leaves and tie'd outputs.
+void run_overhead() {
+    dev::DeviceBackend be;
+    const std::size_t n = 1024;
+    SplitMix64 rng(0x5EED);
+    auto f = random_state(3, n, rng);
+    StateSet u = state_conservative(EosSpec(), 3, leaves_of(f));
+    std::vector<dev::DeviceVector> dv;
+    dev::Residency res;
+    for (auto& v : f) {
+        dv.emplace_back(v.precision(), v.size());
+        dv.back().upload(v);
+    }
+    for (std::size_t i = 0; i < f.size(); ++i) res.bind(f[i], dv[i]);
+    be.residency = &res;
+    std::vector<dev::DeviceVector> fo, jo;
+    for (int i = 0; i < 15; ++i) fo.emplace_back(Precision::f64, n);
+    for (int i = 0; i < 75; ++i) jo.emplace_back(Precision::f64, n);
+    dev::Tie tf, tj;
+    for (auto& o : fo) tf.dests.push_back(&o);
+    for (auto& o : jo) tj.dests.push_back(&o);
+    auto time = [&](const char* what, auto&& call) {
+        for (int i = 0; i < 50; ++i) call();
+        const int reps = 2000;
+        auto t0 = std::chrono::steady_clock::now();
+        for (int i = 0; i < reps; ++i) call();
+        const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        std::printf("{\"call\": \"%s\", \"n\": %zu, \"us_per_call\": %.2f}\n", what, n,
+                    s / reps * 1e6);
+    };
+    time("evaluate_block(inviscid_flux), resident, tie, synchronous", [&] {
+        dev::evaluate_block(be, inviscid_flux(u), tf);
+    });
+    time("evaluate_block_cfl(jacobian), resident, tie", [&] {
+        (void)dev::evaluate_block_cfl(be, inviscid_flux_jacobian(u), tj);
+    });
+    volatile std::size_t sink = 0;
+    time("build the tree inviscid_flux(u) only (reference code)", [&] {
+        sink = sink + inviscid_flux(u).block_rows();
+    });
+    time("build the tree inviscid_flux_jacobian(u) only", [&] {
+        sink = sink + inviscid_flux_jacobian(u).block_rows();
+    });
+    {
+        BlockExpr J = inviscid_flux_jacobian(u);
+        std::vector<Expr> items;
+        for (std::size_t r = 0; r < J.block_rows(); ++r)
+            for (std::size_t c = 0; c < J.block_cols(); ++c) items.push_back(J.item(r, c).as_expr());
+        std::vector<Precision> dests(items.size(), Precision::f64);
+        time("block_key of the Jacobian block only", [&] {
+            sink = sink + dev::block_key(items, dests, 15, 5, nullptr).size();
+        });
+        const std::string key = dev::block_key(items, dests, 15, 5, nullptr);
+        time("fvb_lookup of the Jacobian key only", [&] {
+            fvb_kernel k;
+            sink = sink + fvb_lookup(key.c_str(), &k);
+        });
+    }
+    dev::DeviceBackend ab = be;
+    ab.synchronize = false;
+    time("evaluate_block(inviscid_flux), resident, tie, asynchronous", [&] {
+        dev::evaluate_block(ab, inviscid_flux(u), tf);
+    });
+    cudaDeviceSynchronize();
+}
+
 int main(int argc, char** argv) {
     const std::string mode = argc > 1 ? argv[1] : "keys";
+    if (mode == "overhead") {
+        run_overhead();
+        return 0;
+    }
     if (mode == "perf") {
         run_perf(argc > 2 ? std::strtoull(argv[2], nullptr, 10) : 20000000ull);
         return 0;
