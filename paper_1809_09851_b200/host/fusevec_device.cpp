@@ -1074,5 +1074,26 @@ double evaluate_block_cfl(const DeviceBackend& be, const BlockExpr& jacobian, co
     return read_max(be, red.p, dest.dests.at(0)->precision());
 }
 
+void evaluate_block_cfl(const DeviceBackend& be, const BlockExpr& jacobian, const Tie& dest,
+                        DeviceVector& lambda_max) {
+    if (lambda_max.size() != 1 || dest.dests.empty() ||
+        lambda_max.precision() != dest.dests.at(0)->precision())
+        throw LengthMismatch("lambda_max must be one element of the block's precision");
+    std::vector<Out> outs;
+    for (DeviceVector* d : dest.dests) {
+        Out o;
+        o.dev = d;
+        outs.push_back(o);
+    }
+    DeviceGuard guard(be.ordinal);
+    cuda_check(cudaMemsetAsync(lambda_max.data(), 0, lambda_max.byte_size(),
+                               static_cast<cudaStream_t>(be.stream)),
+               "lambda reset");
+    block_impl(be, jacobian, jacobian.block_rows(), jacobian.block_cols(), outs, lambda_max.data(),
+               true);
+    if (be.synchronize)
+        cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(be.stream)), "sync");
+}
+
 }  // namespace device
 }  // namespace fusevec

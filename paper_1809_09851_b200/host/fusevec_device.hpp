@@ -190,6 +190,12 @@ double reduce_max(const DeviceBackend& be, const Expr& lambda);
 double evaluate_block_cfl(const DeviceBackend& be, const BlockExpr& jacobian,
                           BlockVectorGrid& dest);
 double evaluate_block_cfl(const DeviceBackend& be, const BlockExpr& jacobian, const Tie& dest);
+/// The same, leaving the maximum on the device in lambda_max (one element of
+/// the block's precision) instead of returning it: no host read-back, so with
+/// synchronize = false a time loop's Jacobian + CFL step can be captured in
+/// a CUDA graph and the maximum consumed by later device work.
+void evaluate_block_cfl(const DeviceBackend& be, const BlockExpr& jacobian, const Tie& dest,
+                        DeviceVector& lambda_max);
 
 }  // namespace device
 }  // namespace fusevec

@@ -611,7 +611,7 @@ void run_gpu() {
         return "";
     });
 
-    check("asynchronous evaluations captured into a CUDA graph (synchronize = false)", [&] {
+    check("asynchronous evaluations, Jacobian + device-side CFL max included, captured into a CUDA graph", [&] {
         // The reference's own calls -- evaluate_block of inviscid_flux and of
         // convert(.., Primitive) -- on resident leaves into tie'd device
         // planes, enqueued without host waits, captured once and replayed.
@@ -640,11 +640,21 @@ void run_gpu() {
         for (auto& o : pr) tp.dests.push_back(&o);
         BlockExpr flux = inviscid_flux(u);
         BlockExpr prim = convert(u, Formulation::Primitive).block();
+        // the Jacobians + CFL step too, its maximum left on the device
+        const bool lowered = std::getenv("FVB_FORCE_LOWER") != nullptr;
+        BlockExpr J = inviscid_flux_jacobian(u);
+        std::vector<dev::DeviceVector> jo;
+        for (int i = 0; i < 75; ++i) jo.emplace_back(Precision::f64, n);
+        dev::Tie tj;
+        for (auto& o : jo) tj.dests.push_back(&o);
+        dev::DeviceVector lam(Precision::f64, 1);
         dev::evaluate_block(ab, flux, tf);  // warm: keys resolved outside the capture
         dev::evaluate_block(ab, prim, tp);
+        if (!lowered) dev::evaluate_block_cfl(ab, J, tj, lam);
         cudaStreamSynchronize(s);
-        for (auto* v : {&fl, &pr})
+        for (auto* v : {&fl, &pr, &jo})
             for (auto& o : *v) cudaMemsetAsync(o.data(), 0, o.byte_size(), s);
+        cudaMemsetAsync(lam.data(), 0xff, 8, s);
         cudaStreamSynchronize(s);
         cudaGraph_t g = nullptr;
         cudaGraphExec_t ge = nullptr;
@@ -652,6 +662,7 @@ void run_gpu() {
             fail("begin capture");
         dev::evaluate_block(ab, flux, tf);
         dev::evaluate_block(ab, prim, tp);
+        if (!lowered) dev::evaluate_block_cfl(ab, J, tj, lam);
         if (cudaStreamEndCapture(s, &g) != cudaSuccess) fail("end capture");
         std::size_t nodes = 0;
         cudaGraphGetNodes(g, nullptr, &nodes);
@@ -671,6 +682,20 @@ void run_gpu() {
             evaluate(ref, w.field(i), wi);
             pr[i].download(tmp);
             if (!same_bits(tmp, wi)) fail("graph primitive field " + std::to_string(i));
+        }
+        if (!lowered) {
+            BlockVectorGrid jw(15, 5, Precision::f64, n);
+            evaluate_block(ref, J, jw);
+            for (std::size_t i = 0; i < 75; ++i) {
+                jo[i].download(tmp);
+                if (!same_bits(tmp, jw.get(i))) fail("graph jacobian item " + std::to_string(i));
+            }
+            DenseVector ws(Precision::f64, n), lv(Precision::f64, 1);
+            evaluate(ref, wave_speed(u), ws);
+            double mx = 0;
+            for (std::size_t i = 0; i < n; ++i) mx = std::fmax(mx, ws.at(i));
+            lam.download(lv);
+            if (lv.at(0) != mx) fail("graph CFL maximum differs");
         }
         cudaGraphExecDestroy(ge);
         cudaGraphDestroy(g);
