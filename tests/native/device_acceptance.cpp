@@ -1059,6 +1059,40 @@ void run_overhead() {
         dev::evaluate_block(ab, inviscid_flux(u), tf);
     });
     cudaDeviceSynchronize();
+    // one time step -- flux, conversion, Jacobians + CFL max on the device --
+    // as reference-API calls, and the same step captured once as a CUDA graph
+    cudaStream_t s = nullptr;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    ab.stream = s;
+    std::vector<dev::DeviceVector> po;
+    for (int i = 0; i < 5; ++i) po.emplace_back(Precision::f64, n);
+    dev::Tie tp;
+    for (auto& o : po) tp.dests.push_back(&o);
+    dev::DeviceVector lam(Precision::f64, 1);
+    BlockExpr F = inviscid_flux(u), P = convert(u, Formulation::Primitive).block(),
+              J = inviscid_flux_jacobian(u);
+    auto step = [&] {
+        dev::evaluate_block(ab, F, tf);
+        dev::evaluate_block(ab, P, tp);
+        dev::evaluate_block_cfl(ab, J, tj, lam);
+    };
+    time("time step as 3 asynchronous reference-API calls (trees prebuilt)", [&] {
+        step();
+        cudaStreamSynchronize(s);
+    });
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    step();
+    cudaStreamEndCapture(s, &g);
+    cudaGraphInstantiate(&ge, g, 0);
+    time("the same time step replayed as one CUDA graph", [&] {
+        cudaGraphLaunch(ge, s);
+        cudaStreamSynchronize(s);
+    });
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    cudaStreamDestroy(s);
 }
 
 int main(int argc, char** argv) {
