@@ -463,6 +463,35 @@ void run_gpu() {
         return "";
     });
 
+    check("f32 flux, primitive conversion and sound speed on device, d = 1..3, bitwise", [&] {
+        SplitMix64 rng(0xF32);
+        for (std::size_t d = 1; d <= 3; ++d) {
+            const std::size_t n = 10007;
+            auto f = random_state(d, n, rng, Precision::f32);
+            StateSet u = state_conservative(EosSpec(), d, leaves_of(f));
+            BlockVectorGrid want(d + 2, d, Precision::f32, n), got(d + 2, d, Precision::f32, n);
+            evaluate_block(ref, inviscid_flux(u), want);
+            dev::evaluate_block(be, inviscid_flux(u), got);
+            for (std::size_t i = 0; i < (d + 2) * d; ++i)
+                if (!same_bits(want.get(i), got.get(i))) fail("f32 flux d=" + std::to_string(d));
+            StateSet w = convert(u, Formulation::Primitive);
+            std::vector<DenseVector> pd;
+            for (std::size_t i = 0; i < d + 2; ++i) pd.emplace_back(Precision::f32, n);
+            BlockColVector pv(std::move(pd));
+            dev::evaluate_block(be, w.block(), pv);
+            for (std::size_t i = 0; i < d + 2; ++i) {
+                DenseVector wi(Precision::f32, n);
+                evaluate(ref, w.field(i), wi);
+                if (!same_bits(wi, pv.get(i))) fail("f32 primitive field " + std::to_string(i));
+            }
+            DenseVector cw(Precision::f32, n), cg(Precision::f32, n);
+            evaluate(ref, derived_c(u), cw);
+            dev::evaluate(be, derived_c(u), cg);
+            if (!same_bits(cw, cg)) fail("f32 sound speed d=" + std::to_string(d));
+        }
+        return "";
+    });
+
     check("criterion 6 worked instance on device: column 0 = [2,4,4,4,16]", [&] {
         DenseVector rho({2.0}), mx({2.0}), my({4.0}), mz({4.0}), rhoE({14.0});
         StateSet u = state_conservative(EosSpec(), 3, rho, mx, my, mz, rhoE);
