@@ -463,7 +463,7 @@ void run_gpu() {
         return "";
     });
 
-    check("f32 flux, primitive conversion and sound speed on device, d = 1..3, bitwise", [&] {
+    check("f32 flux (conservative and primitive states), conversion and sound speed on device, d = 1..3", [&] {
         SplitMix64 rng(0xF32);
         for (std::size_t d = 1; d <= 3; ++d) {
             const std::size_t n = 10007;
@@ -488,6 +488,15 @@ void run_gpu() {
             evaluate(ref, derived_c(u), cw);
             dev::evaluate(be, derived_c(u), cg);
             if (!same_bits(cw, cg)) fail("f32 sound speed d=" + std::to_string(d));
+            // the flux of a primitive-formulation state (fluid.cpp:290-298)
+            std::vector<Expr> pl;
+            for (std::size_t i = 0; i < d + 2; ++i) pl.push_back(leaf(pv.get(i)));
+            StateSet up = state_primitive(EosSpec(), d, pl);
+            BlockVectorGrid fw(d + 2, d, Precision::f32, n), fg(d + 2, d, Precision::f32, n);
+            evaluate_block(ref, inviscid_flux(up), fw);
+            dev::evaluate_block(be, inviscid_flux(up), fg);
+            for (std::size_t i = 0; i < (d + 2) * d; ++i)
+                if (!same_bits(fw.get(i), fg.get(i))) fail("primitive-state flux d=" + std::to_string(d));
         }
         return "";
     });
