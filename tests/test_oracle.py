@@ -338,3 +338,24 @@ def test_eos_matches_reference(orc, ref, prec):
         want_p, want_T = ref.eos(rho, e, cp=cp, cv=cv)
         got_p, got_T = orc.eos(rho, e, gas=orc.gas(cp, cv))
         assert got_p.tobytes() == want_p.tobytes() and got_T.tobytes() == want_T.tobytes()
+
+
+# Gases with awkward rational constants: gamma - 1 = R/cv and gamma = cp/cv
+# are then inexact doubles, so the narrowing and the operation order of
+# every block are exercised (fluid.cpp:40-53).
+RANDOM_GASES = [((7, 2), (5, 2)), ((5, 2), (3, 2)), ((9, 7), (1, 1)), ((13, 3), (11, 5)),
+                ((100, 33), (2, 1)), ((31, 10), (7, 3))]
+
+
+@pytest.mark.parametrize("cp,cv", RANDOM_GASES)
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_blocks_match_reference_for_many_gases(orc, ref, cp, cv, prec):
+    g = orc.gas(cp=cp, cv=cv)
+    for dim in (1, 3):
+        s = orc.random_state(dim, 1031, seed=sum(cp) + 7 * sum(cv), prec=prec)
+        mine = orc.flux(dim, s, gas=g) + orc.cons2prim(dim, s, gas=g)
+        theirs = ref.flux(dim, s, cp=cp, cv=cv) + ref.cons2prim(dim, s, cp=cp, cv=cv)
+        assert all(a.tobytes() == b.tobytes() for a, b in zip(mine, theirs)), (cp, cv, dim)
+        jm, lm = orc.jacobian(dim, s, gas=g)
+        jt, lt = ref.jacobian(dim, s, cp=cp, cv=cv)
+        assert all(a.tobytes() == b.tobytes() for a, b in zip(jm, jt)) and lm == lt

@@ -671,3 +671,22 @@ def test_eos_bitwise(cuda, orc, prec):
     N.check(N.lib().fvb_eos(None, PREC[prec], n, d_rho.data_ptr(), d_e.data_ptr(), None,
                             T_only.data_ptr(), torch.cuda.current_stream().cuda_stream))
     assert same_bits(to_host([T_only])[0], orc.eos(rho, e)[1])
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_many_gases_bitwise(cuda, orc, prec):
+    # the device blocks under the gases test_oracle.py pins to the reference
+    from tests.test_oracle import RANDOM_GASES
+    for cp, cv in RANDOM_GASES:
+        g = fvb.Gas(cp[0], cp[1], cv[0], cv[1])
+        og = orc.gas(cp=cp, cv=cv)
+        for dim in (1, 2, 3):
+            s_np = orc.random_state(dim, 4099, seed=sum(cp) + dim, prec=prec)
+            s = to_dev(s_np, cuda)
+            assert all_same(to_host(fvb.flux(s, dim, gas=g)), orc.flux(dim, s_np, gas=og))
+            assert all_same(to_host(fvb.cons2prim(s, dim, gas=g)),
+                            orc.cons2prim(dim, s_np, gas=og))
+            j, lam = fvb.jacobian(s, dim, gas=g)
+            j_np, lam_np = orc.jacobian(dim, s_np, gas=og)
+            assert all_same(to_host(j), j_np), (cp, cv, dim)
+            assert same_bits(lam.cpu().numpy(), np.asarray(lam_np, NP[prec]))
