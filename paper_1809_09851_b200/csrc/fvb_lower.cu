@@ -46,7 +46,7 @@
 namespace fvb {
 namespace {
 
-constexpr int kMaxArgs = 128;
+constexpr int kMaxArgs = 256;  // 2 KB of plane pointers per launch
 constexpr int kThreads = 256;
 constexpr int kPerThread = 4;
 

@@ -661,6 +661,25 @@ bool reads_earlier_destination(const DeviceBackend& be, const std::vector<Expr>&
     return false;
 }
 
+// A block with more planes than one launch's argument block carries runs as
+// several fused kernels over halves of its items.  No item reads another's
+// destination (block_impl checks that first), so the split is exact.  A
+// single item that still has no kernel is unsupported.
+void run_in_parts(const DeviceBackend& be, const std::vector<Expr>& items,
+                  const std::vector<Out>& outs, std::size_t n) {
+    Plan p;
+    if (try_plan(items, outs, items.size(), 1, &p)) {
+        run(be, p, n, nullptr);
+        return;
+    }
+    if (items.size() == 1) unsupported(items);
+    const std::size_t h = items.size() / 2;
+    run_in_parts(be, std::vector<Expr>(items.begin(), items.begin() + long(h)),
+                 std::vector<Out>(outs.begin(), outs.begin() + long(h)), n);
+    run_in_parts(be, std::vector<Expr>(items.begin() + long(h), items.end()),
+                 std::vector<Out>(outs.begin() + long(h), outs.end()), n);
+}
+
 // Shared body of the evaluate_block overloads.
 void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, std::size_t cols,
                 const std::vector<Out>& dests_in, void* red, bool need_reduce) {
@@ -748,7 +767,9 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
             plan = std::move(alt);
             copies = std::move(stripped);
         } else if (!whole) {
-            unsupported(items);
+            if (need_reduce) unsupported(items);
+            run_in_parts(be, items, outs, n);
+            return;
         }
     }
     if (need_reduce && !plan.k.reduce)

@@ -622,6 +622,29 @@ void run_gpu() {
         return "";
     });
 
+    check("a block wider than one launch (300 planes) runs as fused parts", [&] {
+        SplitMix64 rng(71);
+        const std::size_t n = 3001, items = 100;
+        std::vector<DenseVector> in;
+        for (std::size_t i = 0; i < 2 * items; ++i)
+            in.push_back(testutil::make_vec(Precision::f64, n, rng));
+        std::vector<BlockItem> bi;
+        for (std::size_t i = 0; i < items; ++i)
+            bi.push_back(BlockItem(leaf(in[2 * i]) * leaf(in[2 * i + 1]) - leaf(in[2 * i])));
+        BlockExpr e(items, 1, bi);
+        std::vector<DenseVector> wd, gd;
+        for (std::size_t i = 0; i < items; ++i) {
+            wd.emplace_back(Precision::f64, n);
+            gd.emplace_back(Precision::f64, n);
+        }
+        BlockColVector want(std::move(wd)), got(std::move(gd));
+        evaluate_block(ref, e, want);
+        dev::evaluate_block(be, e, got);
+        for (std::size_t i = 0; i < items; ++i)
+            if (!same_bits(want.get(i), got.get(i))) fail("item " + std::to_string(i));
+        return "";
+    });
+
     check("column-major blocks and destination grids map items logically", [&] {
         // linear_index (block.hpp:14-18): a ColMajor grid stores item (r, c)
         // at c*nrow + r; items are still matched by (r, c)
