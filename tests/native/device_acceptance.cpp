@@ -622,6 +622,63 @@ void run_gpu() {
         return "";
     });
 
+    check("narrowing rules on device: f32 constants, one rounding into a narrow store", [&] {
+        // test_backend.cpp:122-138
+        DenseVector ones(Precision::f32, 9000);
+        for (std::size_t i = 0; i < 9000; ++i) ones.set(i, 1.0);
+        DenseVector out(Precision::f32, 9000);
+        dev::evaluate(be, leaf(ones) * constant(0.1, leaf(ones)), out);
+        if (out.f32()[0] != 0.1f || static_cast<double>(out.f32()[8999]) == 0.1)
+            fail("f32 constant not narrowed before use");
+        SplitMix64 rng(81);
+        DenseVector x = testutil::make_vec(Precision::f64, 9000, rng, 0.1, 0.9);
+        DenseVector narrow(Precision::f32, 9000), want(Precision::f32, 9000);
+        dev::evaluate(be, leaf(x) * leaf(x) + leaf(x), narrow);  // exact ops: bitwise
+        evaluate(ref, leaf(x) * leaf(x) + leaf(x), want);
+        if (!same_bits(narrow, want)) fail("wide result stored narrow differs");
+        for (std::size_t i = 0; i < 9000; ++i)
+            if (narrow.f32()[i] != static_cast<float>(x.at(i) * x.at(i) + x.at(i)))
+                fail("not a single rounding");
+        return "";
+    });
+
+    check("formulations agree on device: p, v^2 and the flux from either state", [&] {
+        // test_fluid.cpp:213-232 and 331-345, at n = 20000, within 1e-12
+        SplitMix64 rng(404);
+        for (std::size_t d = 1; d <= 3; ++d) {
+            const std::size_t n = 20000;
+            auto f = random_state(d, n, rng);
+            StateSet uc = state_conservative(EosSpec(), d, leaves_of(f));
+            StateSet up = convert(uc, Formulation::Primitive);
+            // the primitive state's fields on the device, then derived from them
+            std::vector<DenseVector> pf;
+            for (std::size_t i = 0; i < d + 2; ++i) pf.emplace_back(Precision::f64, n);
+            BlockColVector pv(std::move(pf));
+            dev::evaluate_block(be, up.block(), pv);
+            std::vector<Expr> pl;
+            for (std::size_t i = 0; i < d + 2; ++i) pl.push_back(leaf(pv.get(i)));
+            StateSet upm = state_primitive(EosSpec(), d, pl);
+            DenseVector pc(Precision::f64, n), pp(Precision::f64, n), vc(Precision::f64, n),
+                vp(Precision::f64, n);
+            dev::evaluate(be, derived_p(uc), pc);
+            dev::evaluate(be, derived_p(upm), pp);
+            dev::evaluate(be, derived_v_mag2(uc), vc);
+            dev::evaluate(be, derived_v_mag2(upm), vp);
+            for (std::size_t i = 0; i < n; ++i)
+                if (!testutil::scalar_close(pc.at(i), pp.at(i), 1e-12) ||
+                    !testutil::scalar_close(vc.at(i), vp.at(i), 1e-12))
+                    fail("derived quantities disagree, d=" + std::to_string(d));
+            BlockVectorGrid fc(d + 2, d, Precision::f64, n), fp(d + 2, d, Precision::f64, n);
+            dev::evaluate_block(be, inviscid_flux(uc), fc);
+            dev::evaluate_block(be, inviscid_flux(upm), fp);
+            for (std::size_t k = 0; k < (d + 2) * d; ++k)
+                for (std::size_t i = 0; i < n; ++i)
+                    if (!testutil::scalar_close(fc.get(k).at(i), fp.get(k).at(i), 1e-12))
+                        fail("primitive and conservative flux disagree, d=" + std::to_string(d));
+        }
+        return "";
+    });
+
     check("a block wider than one launch (300 planes) runs as fused parts", [&] {
         SplitMix64 rng(71);
         const std::size_t n = 3001, items = 100;
