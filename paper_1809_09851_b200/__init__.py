@@ -22,6 +22,7 @@ from .device import (  # noqa: F401
     HostContext,
     axpy_sin,
     cons2prim,
+    csr_matvec_acc,
     emit_source,
     eos,
     flux,

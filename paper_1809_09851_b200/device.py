@@ -206,6 +206,27 @@ def wave_speed_max(state, dim, lam_out=None, lambda_max=None, gas=None, stream=N
     return lam_out, lambda_max
 
 
+def csr_matvec_acc(row_ptr, col_idx, values, x, y, stream=None):
+    """y += A x for a CSR matrix (block.cpp:345-356): row_ptr (rows+1) and
+    col_idx (nnz) int64 CUDA tensors holding the unsigned indices, values
+    float64 (already narrowed to the matrix precision); x and y f32/f64
+    planes.  Each row is summed in stored order in y's precision."""
+    for t, what in ((row_ptr, "row_ptr"), (col_idx, "col_idx")):
+        if not t.is_cuda or t.dtype != torch.int64 or t.dim() != 1:
+            raise N.ArgumentError(N.FVB_EARG, f"{what} must be a 1-D int64 CUDA tensor")
+    if not values.is_cuda or values.dtype != torch.float64 or values.numel() != col_idx.numel():
+        raise N.ArgumentError(N.FVB_EARG, "values must be float64 with one entry per index")
+    (xp,), cols, px = _planes([x], "x")
+    (yp,), rows, py = _planes([y], "y")
+    if row_ptr.numel() != rows + 1:
+        raise N.LengthMismatch(N.FVB_ELEN, f"row_ptr has {row_ptr.numel()} entries for "
+                                           f"{rows} rows")
+    N.check(N.lib().fvb_csr_matvec_acc(py, px, rows, col_idx.numel(), row_ptr.data_ptr(),
+                                       col_idx.data_ptr(), values.data_ptr(), xp, yp,
+                                       _stream(stream)))
+    return y
+
+
 def axpy_sin(x, y, stream=None):
     """y <- 0.5*sin(x+y) in place."""
     ptrs, n, prec = _planes([x, y], "axpy_sin")

@@ -624,10 +624,7 @@ def test_csr_matvec_bitwise(cuda, orc, y_prec, x_prec):
         drp, dci, dv = _csr_to_dev(rp, ci, v, cuda)
         dx = torch.from_numpy(x).to(cuda)
         dy = torch.from_numpy(y0.copy()).to(cuda)
-        N.check(N.lib().fvb_csr_matvec_acc(PREC[y_prec], PREC[x_prec], rows, len(ci),
-                                           drp.data_ptr(), dci.data_ptr(), dv.data_ptr(),
-                                           dx.data_ptr(), dy.data_ptr(),
-                                           torch.cuda.current_stream().cuda_stream))
+        fvb.csr_matvec_acc(drp, dci, dv, dx, dy)
         assert same_bits(to_host([dy])[0], want), rows
 
 
