@@ -70,6 +70,15 @@ def main():
     torch.cuda.empty_cache()
     bidir = link["bidir_each_GBps"]
     ceil_gpts = 1.0 / (96 / (bidir * 1e9)) / 1e9
+    # pageable host planes: the bounce buffers and copy threads
+    pin_in = [t.clone() for t in hin]
+    pin_out = [t.clone() for t in hout]
+    ctx = fvb.HostContext(0)
+    s = timed(lambda: ctx.flux(pin_in, 3, pin_out), reps=3)
+    ctx.close()
+    print(json.dumps({"chunk_points": "default, PAGEABLE host planes", "ms": s * 1e3,
+                      "gpts": n / s / 1e9}), flush=True)
+    del pin_in, pin_out
     for chunk in (1 << 20, 1 << 22, 1 << 24, 0):
         ctx = fvb.HostContext(0, chunk_points=chunk)
         s = timed(lambda: ctx.flux(hin, 3, hout), reps=3)
