@@ -193,7 +193,9 @@ uint64_t chunk_for(const fvb_ctx* ctx, size_t bytes_per_point, uint64_t n) {
     uint64_t c = ctx->chunk_points;
     if (!c) c = (uint64_t(256) << 20) / std::max<size_t>(bytes_per_point, 1);
     c = std::max<uint64_t>(c & ~uint64_t(255), 256);  // keep 32-byte alignment of slot planes
-    return std::min<uint64_t>(c, std::max<uint64_t>(n, 1));
+    // a range shorter than one chunk still strides its slot planes by a
+    // multiple of 256 elements, so every plane keeps the 32-byte residue
+    return std::min<uint64_t>(c, (std::max<uint64_t>(n, 1) + 255) & ~uint64_t(255));
 }
 
 enum class Mem { kPageable, kPinned, kDevice };
