@@ -150,7 +150,9 @@ def test_structural_key_kernels_stay_in_bounds(cuda, orc):
     A.check("structural-key kernels")
 
 
-def test_csr_matvec_stays_in_bounds(cuda):
+@pytest.mark.parametrize("mode", ["row", "warp", "bulk"])
+def test_csr_matvec_stays_in_bounds(cuda, mode, monkeypatch):
+    monkeypatch.setenv("FVB_CSR_MODE", mode)
     A = Arena(cuda)
     rows, cols = 257, 301
     rng = np.random.default_rng(0)
@@ -162,8 +164,12 @@ def test_csr_matvec_stays_in_bounds(cuda):
         vv += list(rng.uniform(-1, 1, len(c)))
         rp[r + 1] = len(ci)
     drp = torch.from_numpy(rp.view(np.int64)).to(cuda)
-    dci = torch.from_numpy(np.array(ci, np.uint64).view(np.int64)).to(cuda)
-    dv = torch.from_numpy(np.array(vv)).to(cuda)
+    # values and indices in guarded planes too, one element off a 16-byte
+    # boundary (the bulk form's head/tail path), checked unchanged after
+    dv = A.inputs_from([np.array(vv)], 1)[0]
+    dci = A.plane(len(ci), 1, 3)
+    dci.view(torch.int64).copy_(torch.from_numpy(np.array(ci, np.uint64).view(np.int64)))
+    A.inputs.append((dci, dci.clone()))
     xh = rng.uniform(-1, 1, cols)
     x = A.inputs_from([xh], 1)[0]
     y = A.plane(rows, 1, 3)

@@ -603,18 +603,28 @@ def stencil7(n):
     return rp, cols[mask].astype(np.uint64), vals[mask].astype(np.float64)
 
 
+@pytest.fixture(params=["auto", "row", "warp", "bulk"])
+def csr_mode(request, monkeypatch):
+    # the library reads FVB_CSR_MODE per call
+    if request.param != "auto":
+        monkeypatch.setenv("FVB_CSR_MODE", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("y_prec,x_prec", [("f64", "f64"), ("f64", "f32"), ("f32", "f64"),
                                            ("f32", "f32")])
-def test_csr_matvec_bitwise(cuda, orc, y_prec, x_prec):
-    # The warp-staged kernel against the oracle (pinned to the reference in
+def test_csr_matvec_bitwise(cuda, orc, y_prec, x_prec, csr_mode):
+    # Every CSR form against the oracle (pinned to the reference in
     # test_oracle.py): rows longer than one staging tile, warps whose range
-    # spans several tiles, empty rows, a ragged last warp, a 7-point
-    # stencil -- and the accumulation into a nonzero y.
+    # spans several tiles, row blocks too long for a bulk stage, empty rows,
+    # a ragged last warp / block, 7-point stencils -- and the accumulation
+    # into a nonzero y.
     from tests.test_oracle import random_csr
     rng = np.random.default_rng(11)
     yt = {"f64": np.float64, "f32": np.float32}
     cases = [random_csr(rng, 1, 1, 1), random_csr(rng, 37, 3000, 1000, 3),
-             random_csr(rng, 4099, 5000, 40, 9), stencil7(48)]
+             random_csr(rng, 4099, 5000, 40, 9), random_csr(rng, 3001, 900, 9, 5),
+             stencil7(48), stencil7(7)]
     for rp, ci, v in cases:
         rows = len(rp) - 1
         cols = int(ci.max()) + 1 if len(ci) else 1
@@ -626,6 +636,26 @@ def test_csr_matvec_bitwise(cuda, orc, y_prec, x_prec):
         dy = torch.from_numpy(y0.copy()).to(cuda)
         fvb.csr_matvec_acc(drp, dci, dv, dx, dy)
         assert same_bits(to_host([dy])[0], want), rows
+
+
+@pytest.mark.parametrize("v_off,c_off", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_csr_matvec_odd_plane_offsets(cuda, orc, v_off, c_off, csr_mode):
+    # values / column indices starting 8 bytes past a 16-byte boundary: the
+    # bulk form's head and tail elements (read from global, not bulk-copied)
+    rng = np.random.default_rng(12)
+    for rp, ci, v in (stencil7(33), stencil7(5)):
+        rows = len(rp) - 1
+        x = rng.uniform(-2, 2, rows)
+        y0 = rng.uniform(-1, 1, rows)
+        want = orc.csr_matvec_acc(rp, ci, v, x, y0)
+        dv = torch.from_numpy(np.concatenate([[np.nan] * v_off, v])).to(cuda)[v_off:]
+        dci = torch.from_numpy(np.concatenate([[2 ** 62] * c_off, ci.view(np.int64)])
+                               .astype(np.int64)).to(cuda)[c_off:]
+        drp = torch.from_numpy(rp.view(np.int64)).to(cuda)
+        assert (dv.data_ptr() % 16 == 8) == bool(v_off) and (dci.data_ptr() % 16 == 8) == bool(c_off)
+        dy = torch.from_numpy(y0.copy()).to(cuda)
+        fvb.csr_matvec_acc(drp, dci, dv, torch.from_numpy(x).to(cuda), dy)
+        assert same_bits(to_host([dy])[0], want), (rows, v_off, c_off)
 
 
 def test_host_path_without_bounce_buffers(cuda):

@@ -8,8 +8,8 @@ Workload: the 7-point Laplacian on an n^3 grid (y += A x, f64), the PDE
 stencil the block layer's matvec serves.  Algorithmic bytes per launch:
 row_ptr 8*(rows+1) + (values + col_idx) 16*nnz + x 8*rows (each element
 once) + y 16*rows (read + write).  Prints one JSON line per kernel variant
-(FVB_CSR_ROWWISE=1 selects the row-per-thread form; run the script once
-with and once without it) and the reference's rate on a bounded sample.
+(FVB_CSR_MODE=row|warp|bulk forces one form; unset = the library's
+own choice) and the reference's rate on a bounded sample.
 Parity: the device y equals the oracle bit for bit.
 """
 
@@ -78,14 +78,15 @@ def main():
         peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     except Exception:
         pass
-    variant = "rowwise" if os.environ.get("FVB_CSR_ROWWISE", "0") not in ("", "0") else "warp"
+    variant = os.environ.get("FVB_CSR_MODE", "") or (
+        "rowwise" if os.environ.get("FVB_CSR_ROWWISE", "0") not in ("", "0") else "auto")
     line = {"kernel": f"csr_{variant}", "grid": f"{a.n}^3", "rows": rows, "nnz": nnz,
             "ms": t * 1e3, "grows_per_s": rows / t / 1e9, "algorithmic_bytes": bytes_,
             "GBps": bytes_ / t / 1e9, "peak_GBps": peak, "frac": bytes_ / t / 1e9 / peak,
             "bitwise_vs_oracle": bitwise, "l2": "flushed between reps"}
     print(json.dumps(line), flush=True)
     ref = oracle.reference()
-    if ref is not None and variant == "warp" and a.ref_n > 0:
+    if ref is not None and variant == "auto" and a.ref_n > 0:
         ts, rnnz = ref.time_csr(a.ref_n, 5)
         rrows = a.ref_n ** 3
         print(json.dumps({"kernel": "reference csr_matvec_acc (serial, 1 core)",
