@@ -150,7 +150,7 @@ def test_structural_key_kernels_stay_in_bounds(cuda, orc):
     A.check("structural-key kernels")
 
 
-@pytest.mark.parametrize("mode", ["row", "warp", "bulk"])
+@pytest.mark.parametrize("mode", ["row", "warp"])
 def test_csr_matvec_stays_in_bounds(cuda, mode, monkeypatch):
     monkeypatch.setenv("FVB_CSR_MODE", mode)
     A = Arena(cuda)
@@ -165,7 +165,7 @@ def test_csr_matvec_stays_in_bounds(cuda, mode, monkeypatch):
         rp[r + 1] = len(ci)
     drp = torch.from_numpy(rp.view(np.int64)).to(cuda)
     # values and indices in guarded planes too, one element off a 16-byte
-    # boundary (the bulk form's head/tail path), checked unchanged after
+    # boundary, checked unchanged after
     dv = A.inputs_from([np.array(vv)], 1)[0]
     dci = A.plane(len(ci), 1, 3)
     dci.view(torch.int64).copy_(torch.from_numpy(np.array(ci, np.uint64).view(np.int64)))

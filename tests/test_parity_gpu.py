@@ -603,7 +603,7 @@ def stencil7(n):
     return rp, cols[mask].astype(np.uint64), vals[mask].astype(np.float64)
 
 
-@pytest.fixture(params=["auto", "row", "warp", "bulk"])
+@pytest.fixture(params=["auto", "row", "warp"])
 def csr_mode(request, monkeypatch):
     # the library reads FVB_CSR_MODE per call
     if request.param != "auto":
@@ -616,7 +616,7 @@ def csr_mode(request, monkeypatch):
 def test_csr_matvec_bitwise(cuda, orc, y_prec, x_prec, csr_mode):
     # Every CSR form against the oracle (pinned to the reference in
     # test_oracle.py): rows longer than one staging tile, warps whose range
-    # spans several tiles, row blocks too long for a bulk stage, empty rows,
+    # spans several tiles, empty rows,
     # a ragged last warp / block, 7-point stencils -- and the accumulation
     # into a nonzero y.
     from tests.test_oracle import random_csr
@@ -640,8 +640,8 @@ def test_csr_matvec_bitwise(cuda, orc, y_prec, x_prec, csr_mode):
 
 @pytest.mark.parametrize("v_off,c_off", [(0, 0), (1, 0), (0, 1), (1, 1)])
 def test_csr_matvec_odd_plane_offsets(cuda, orc, v_off, c_off, csr_mode):
-    # values / column indices starting 8 bytes past a 16-byte boundary: the
-    # bulk form's head and tail elements (read from global, not bulk-copied)
+    # values / column indices starting 8 bytes past a 16-byte boundary
+    # (offset planes a caller may pass through the C ABI)
     rng = np.random.default_rng(12)
     for rp, ci, v in (stencil7(33), stencil7(5)):
         rows = len(rp) - 1

@@ -8,7 +8,7 @@ Workload: the 7-point Laplacian on an n^3 grid (y += A x, f64), the PDE
 stencil the block layer's matvec serves.  Algorithmic bytes per launch:
 row_ptr 8*(rows+1) + (values + col_idx) 16*nnz + x 8*rows (each element
 once) + y 16*rows (read + write).  Prints one JSON line per kernel variant
-(FVB_CSR_MODE=row|warp|bulk forces one form; unset = the library's
+(FVB_CSR_MODE=row|warp forces one form; unset = the library's
 own choice) and the reference's rate on a bounded sample.
 Parity: the device y equals the oracle bit for bit.
 """

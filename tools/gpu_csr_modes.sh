@@ -1,11 +1,9 @@
-# CSR forms on one B200: the CSR parity/bounds tests, then each form and
-# bulk ring shape through tools/csr_bench.py (7-point Laplacian, 256^3).
+# CSR forms on one B200: the CSR parity/bounds tests, then each form through
+# tools/csr_bench.py (7-point Laplacian, 256^3).
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q -k "csr" > gpurun_out/pytest_csr.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_csr.log
 rm -f gpurun_out/csr_modes.jsonl
-FVB_CSR_MODE=warp timeout 300 python tools/csr_bench.py --n 256 --reps 20 --ref-n 0 >> gpurun_out/csr_modes.jsonl 2>> gpurun_out/csr_modes.err
-for shape in "" 16x48 24x48 20x40 8x32; do
-  echo "{\"shape\": \"$shape\"}" >> gpurun_out/csr_modes.jsonl
-  FVB_CSR_MODE=bulk FVB_CSR_BULK=$shape timeout 300 python tools/csr_bench.py --n 256 --reps 20 --ref-n 0 >> gpurun_out/csr_modes.jsonl 2>> gpurun_out/csr_modes.err
+for m in row warp; do
+  FVB_CSR_MODE=$m timeout 300 python tools/csr_bench.py --n 256 --reps 20 --ref-n 0 >> gpurun_out/csr_modes.jsonl 2>> gpurun_out/csr_modes.err
 done
