@@ -9,6 +9,6 @@ if [ "$1" = probe ]; then
 fi
 for args in "--config flux3d --prec f64" "--config flux3d --prec f32" "--config cons2prim1d --prec f64" "--config cons2prim1d --prec f32" \
             "--config jacobian3d --prec f64 --no-e2e" "--config jacobian3d --prec f32 --no-e2e" \
-            "--config axpy --prec f64 --steps 1000" "--config vmag2 --prec f64" "--config vmag2 --prec f32"; do
+            "--config axpy --prec f64 --steps 300" "--config axpy --prec f64 --steps 1000 --l2-warm" "--config vmag2 --prec f64" "--config vmag2 --prec f32"; do
   timeout 600 python bench.py $args --out $OUT > /dev/null 2>> gpurun_out/configs.err
 done
