@@ -200,7 +200,7 @@ def cpu_threads():
 
 def end_to_end(a, fvb, ins, n, n_in, n_out, dim, dt, esize, local, dist, world, dev, torch):
     """Same metric through the host-buffer C-ABI call (fvb_flux_host /
-    fvb_jacobian_host): inputs copied from pinned host memory and every
+    fvb_jacobian_host / fvb_launch_host): inputs copied from pinned host memory and every
     computed output plane copied back, all inside the timed region.  The
     flux's row 0 (bit-for-bit the momentum inputs) is copied host-side by the
     library instead of crossing PCIe; it is counted separately.
@@ -215,17 +215,30 @@ def end_to_end(a, fvb, ins, n, n_in, n_out, dim, dt, esize, local, dist, world, 
         n = min(n, a.e2e_points)
     torch.cuda.empty_cache()
     host_in = torch.empty((n_in, n), dtype=dt).pin_memory()
-    for i, t in enumerate(ins):
+    for i, t in enumerate(ins[:n_in]):  # (v_mag2 reads rho and m only)
         host_in[i].copy_(t[:n])
     host_in = list(host_in.unbind(0))
     host_out = list(torch.empty((n_out, n), dtype=dt).pin_memory().unbind(0))
     ctx = fvb.HostContext(local)
+    kernel = planes = None
+    if a.config in LAUNCH_HOST_PATTERN:
+        # blocks without a named host-buffer call: the registry kernel of the
+        # reference's tree through fvb_launch_host (argument block: outputs,
+        # then the leaves in slot order)
+        kernel = fvb.lookup(registry_key(fvb, LAUNCH_HOST_PATTERN[a.config] + "_" + a.prec))
+        assert kernel.n_outputs == n_out and kernel.n_inputs == n_in, a.config
+        slots = [None] * n_in
+        for i in range(n_in):
+            slots[kernel.in_slot[i]] = host_in[i]
+        planes = host_out + slots
 
     def e2e_step():
         if a.config == "flux3d":
             ctx.flux(host_in, dim, host_out)
-        else:
+        elif a.config == "jacobian3d":
             ctx.jacobian(host_in, dim, host_out)
+        else:
+            ctx.launch(kernel, planes, n)
 
     e2e_step()  # warm (staging allocation)
     if dist is not None:
@@ -247,7 +260,26 @@ def end_to_end(a, fvb, ins, n, n_in, n_out, dim, dt, esize, local, dist, world, 
             "host_passthrough_bytes_per_step": world * n * passthrough * esize,
             "ms_per_step": e2e_s * 1e3, "host_memory": "pinned", "steps": a.e2e_steps,
             "points_per_rank": n,
-            "path": "fvb_flux_host" if a.config == "flux3d" else "fvb_jacobian_host"}
+            "path": {"flux3d": "fvb_flux_host", "jacobian3d": "fvb_jacobian_host"}.get(
+                a.config, "fvb_launch_host")}
+
+
+# configs whose e2e runs the registry kernel through fvb_launch_host
+LAUNCH_HOST_PATTERN = {"cons2prim1d": "cons2prim_c1", "vmag2": "v_mag23"}
+# the default gas's named constants (EosSpec(): gamma = 7/5, R = 1, cv = 5/2)
+_GAS_CONSTS = {"half": 0.5, "gm1": 0.4, "gamma": 1.4, "zero": 0.0, "one": 1.0, "cv": 2.5}
+
+
+def registry_key(fvb, name):
+    """The structural key of registry pattern `name` with the default gas's
+    constants filled in (the key the reference renders for its own tree:
+    C<p><16 hex digits of the double>;)."""
+    import re
+    import struct
+    pat = dict(fvb.patterns())[name]
+    return re.sub(r"C([sd])#(\w+);",
+                  lambda m: "C%s%016x;" % (m.group(1), struct.unpack(
+                      "<Q", struct.pack("<d", _GAS_CONSTS[m.group(2)]))[0]), pat)
 
 
 
@@ -383,7 +415,7 @@ def device_run(a, rank, world, local):
 
     # ---- end to end through the host-buffer C-ABI call -----------------------------
     e2e = None
-    if not a.no_e2e and a.config in ("flux3d", "jacobian3d"):
+    if not a.no_e2e and a.config != "axpy":
         try:
             e2e = end_to_end(a, fvb, ins, n, n_in, n_out, dim, dt, esize, local, dist, world,
                              dev, torch)
