@@ -394,40 +394,58 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
     return FVB_OK;
 }
 
-// Host threads copying pass-through items: output j < PASS is bit-for-bit
-// input plane 1 + j (the flux's row 0 is the momentum fields themselves,
-// include/fusevec/fluid.hpp:168-169).  The host already holds those bytes,
-// so they are copied host-side, concurrently with the device pipeline,
-// instead of crossing PCIe twice.  Joined on every exit path.
-struct PassThrough {
+// Host-side outputs, written by host threads concurrently with the device
+// pipeline instead of crossing PCIe:
+//  - pass-through items: output j < PASS is bit-for-bit input plane 1 + j
+//    (the flux's row 0 is the momentum fields themselves,
+//    include/fusevec/fluid.hpp:168-169); the host already holds those bytes;
+//  - constant items (the Jacobian's 0 / 1 / gamma-1 entries, 30 of 75 in
+//    3-D): every element is the same value of T, filled in place.
+// Joined on every exit path.
+struct HostJob {
+    char* dst;
+    const char* src;  // nullptr: fill with `fill` (the bits of one T)
+    uint64_t fill;
+};
+
+template <class T>
+struct HostSide {
     std::vector<std::thread> workers;
-    PassThrough(const void* const* in, void* const* out, int pass, size_t bytes) {
-        if (pass <= 0 || bytes == 0) return;
+    HostSide(const std::vector<HostJob>& jobs, size_t bytes) {
+        if (jobs.empty() || bytes == 0) return;
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         const unsigned nt = std::min(8u, std::max(1u, hw / 2));
-        const size_t total = size_t(pass) * bytes;
-        const size_t per = (total + nt - 1) / nt;
-        auto copy = [=](size_t lo, size_t hi) {
+        const size_t total = jobs.size() * bytes;
+        const size_t per = ((total + nt - 1) / nt + 63) & ~size_t(63);  // whole elements
+        auto work = [jobs, bytes](size_t lo, size_t hi) {
             while (lo < hi) {
-                const size_t plane = lo / bytes, at = lo % bytes;
+                const HostJob& j = jobs[lo / bytes];
+                const size_t at = lo % bytes;
                 const size_t len = std::min(hi - lo, bytes - at);
-                std::memcpy(static_cast<char*>(out[plane]) + at,
-                            static_cast<const char*>(in[1 + plane]) + at, len);
+                if (j.src) {
+                    std::memcpy(j.dst + at, j.src + at, len);
+                } else if (j.fill == 0) {
+                    std::memset(j.dst + at, 0, len);
+                } else {
+                    T v;
+                    std::memcpy(&v, &j.fill, sizeof v);
+                    std::fill_n(reinterpret_cast<T*>(j.dst + at), len / sizeof(T), v);
+                }
                 lo += len;
             }
         };
         try {
-            for (unsigned t = 0; t < nt; ++t) {
+            for (unsigned t = 0; t < nt && size_t(t) * per < total; ++t) {
                 const size_t lo = size_t(t) * per;
-                workers.emplace_back(copy, lo, std::min(total, lo + per));
+                workers.emplace_back(work, lo, std::min(total, lo + per));
             }
-        } catch (...) {  // no threads to be had: copy on the calling thread
+        } catch (...) {  // no threads to be had: on the calling thread
             for (auto& w : workers) w.join();
             workers.clear();
-            copy(0, total);
+            work(0, total);
         }
     }
-    ~PassThrough() {
+    ~HostSide() {
         for (auto& w : workers) w.join();
     }
 };
@@ -452,7 +470,7 @@ fvb_status read_lambda(fvb_ctx* ctx, double* lambda_max) {
     return FVB_OK;
 }
 
-template <class Op, class T, bool RED, bool TUNE, int PASS = 0>
+template <class Op, class T, bool RED, bool TUNE, int PASS = 0, bool FILL = false>
 fvb_status pipeline(fvb_ctx* ctx, const void* const* in, void* const* out, uint64_t n,
                     const Consts<T>& k, double* lambda_max) {
     constexpr int NIN = Op::NIN, NOUT = Op::NOUT;
@@ -478,14 +496,29 @@ fvb_status pipeline(fvb_ctx* ctx, const void* const* in, void* const* out, uint6
     std::vector<Arg> args;
     for (int i = 0; i < NIN; ++i)
         args.push_back({static_cast<char*>(const_cast<void*>(in[i])), nullptr, sizeof(T), false});
+    std::vector<HostJob> host_side;
     for (int j = 0; j < NOUT; ++j) {
-        // pass-through outputs are copied host-side; the kernel's copy of
-        // them lands in a device scratch slot
-        Arg a{j < PASS ? nullptr : static_cast<char*>(out[j]), nullptr, sizeof(T), true};
-        a.scratch = j < PASS;
+        // pass-through and constant outputs are written host-side; the
+        // kernel's copy of them lands in a device scratch slot
+        bool on_host = j < PASS;
+        if (on_host) {
+            host_side.push_back({static_cast<char*>(out[j]),
+                                 static_cast<const char*>(in[1 + j]), 0});
+        }
+        if constexpr (FILL) {
+            T v;
+            if (!on_host && Op::constant_item(j, k, &v)) {
+                uint64_t bits = 0;
+                std::memcpy(&bits, &v, sizeof v);
+                host_side.push_back({static_cast<char*>(out[j]), nullptr, bits});
+                on_host = true;
+            }
+        }
+        Arg a{on_host ? nullptr : static_cast<char*>(out[j]), nullptr, sizeof(T), true};
+        a.scratch = on_host;
         args.push_back(a);
     }
-    PassThrough pass(in, out, PASS, size_t(n) * sizeof(T));
+    HostSide<T> host_writes(host_side, size_t(n) * sizeof(T));
     fvb_status st = staged(ctx, args, n, [&](void* const* d, uint64_t cnt, cudaStream_t s) {
         const T* din[NIN];
         T* dout[NOUT > 0 ? NOUT : 1];
@@ -499,21 +532,22 @@ fvb_status pipeline(fvb_ctx* ctx, const void* const* in, void* const* out, uint6
 }
 
 // PASS_DIM: the first d outputs are pass-through copies of inputs 1..d.
+// FILL: outputs the op reports as constant items are filled host-side.
 template <template <class, int> class OpT, bool RED, class T, bool TUNE3 = false,
-          bool PASS_DIM = false>
+          bool PASS_DIM = false, bool FILL = false>
 fvb_status pipeline_dim(fvb_ctx* ctx, const fvb_gas* gas, uint32_t dim, const void* const* in,
                         void* const* out, uint64_t n, double* lambda_max) {
     const auto k = make_consts<T>(gas);
     switch (dim) {
         case 1:
-            return pipeline<OpT<T, 1>, T, RED, false, PASS_DIM ? 1 : 0>(ctx, in, out, n, k,
-                                                                        lambda_max);
+            return pipeline<OpT<T, 1>, T, RED, false, PASS_DIM ? 1 : 0, FILL>(ctx, in, out, n, k,
+                                                                              lambda_max);
         case 2:
-            return pipeline<OpT<T, 2>, T, RED, false, PASS_DIM ? 2 : 0>(ctx, in, out, n, k,
-                                                                        lambda_max);
+            return pipeline<OpT<T, 2>, T, RED, false, PASS_DIM ? 2 : 0, FILL>(ctx, in, out, n, k,
+                                                                              lambda_max);
         default:
-            return pipeline<OpT<T, 3>, T, RED, TUNE3, PASS_DIM ? 3 : 0>(ctx, in, out, n, k,
-                                                                        lambda_max);
+            return pipeline<OpT<T, 3>, T, RED, TUNE3, PASS_DIM ? 3 : 0, FILL>(ctx, in, out, n, k,
+                                                                              lambda_max);
     }
 }
 
@@ -590,14 +624,19 @@ fvb_status fvb_jacobian_host(fvb_ctx* ctx, const fvb_gas* gas, uint32_t dim, uin
                              double* lambda_max) {
     return guarded([&]() -> fvb_status {
         if (fvb_status st = check(ctx, gas, dim, prec)) return st;
+        // the constant entries are filled host-side (JacobianOp::constant_item)
         if (prec == FVB_F64) {
             if (lambda_max)
-                return pipeline_dim<JacobianOp, true, double>(ctx, gas, dim, in, out, n, lambda_max);
-            return pipeline_dim<JacobianOp, false, double>(ctx, gas, dim, in, out, n, nullptr);
+                return pipeline_dim<JacobianOp, true, double, false, false, true>(
+                    ctx, gas, dim, in, out, n, lambda_max);
+            return pipeline_dim<JacobianOp, false, double, false, false, true>(ctx, gas, dim, in,
+                                                                              out, n, nullptr);
         }
         if (lambda_max)
-            return pipeline_dim<JacobianOp, true, float>(ctx, gas, dim, in, out, n, lambda_max);
-        return pipeline_dim<JacobianOp, false, float>(ctx, gas, dim, in, out, n, nullptr);
+            return pipeline_dim<JacobianOp, true, float, false, false, true>(ctx, gas, dim, in,
+                                                                            out, n, lambda_max);
+        return pipeline_dim<JacobianOp, false, float, false, false, true>(ctx, gas, dim, in, out,
+                                                                         n, nullptr);
     });
 }
 

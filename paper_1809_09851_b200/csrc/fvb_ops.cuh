@@ -277,20 +277,43 @@ struct JacobianOp {
         s.lam = sqrt(msq / (rho * rho)) + sound_speed(k, rho, p);
         return s;
     }
+    // The items that are constants whatever the state (30 of the 75 in 3-D:
+    // row 0, the momentum rows' last column, and the momentum entries with
+    // no term): their value, shared by the kernel and the host-buffer path
+    // (which fills them host-side instead of shipping them over PCIe).
+    __host__ __device__ __forceinline__ static bool constant_item(int item, const Consts<T>& k,
+                                                                  T* v) {
+        const int dir = item / (W * W);
+        const int r = (item / W) % W;
+        const int c = item % W;
+        if (r == 0) {
+            *v = c == 1 + dir ? k.one : k.zero;
+            return true;
+        }
+        if (r <= D && c == W - 1) {
+            *v = r - 1 == dir ? k.gm1 : k.zero;
+            return true;
+        }
+        if (r <= D && c != 0 && r - 1 != c - 1 && c - 1 != dir && r - 1 != dir) {
+            *v = k.zero;
+            return true;
+        }
+        return false;
+    }
     __device__ __forceinline__ static T out(const State& s, int item, const Consts<T>& k) {
+        T cv;
+        if (constant_item(item, k, &cv)) return cv;
         const int dir = item / (W * W);
         const int r = (item / W) % W;
         const int c = item % W;
         const T uk = s.u[dir];
-        if (r == 0) return c == 1 + dir ? k.one : k.zero;
         if (r <= D) {
             const int i = r - 1;
             if (c == 0) return i == dir ? s.phi - s.u[i] * uk : -(s.u[i] * uk);
-            if (c == W - 1) return i == dir ? k.gm1 : k.zero;
             const int j = c - 1;
-            // Present terms in the fixed order of A.3.
+            // Present terms in the fixed order of A.3 (at least one present:
+            // the term-free entries are constant items).
             const bool t0 = (i == j), t1 = (j == dir), t2 = (i == dir);
-            if (!t0 && !t1 && !t2) return k.zero;
             T acc;
             if (t0) acc = uk;
             if (t1) acc = t0 ? acc + s.u[i] : s.u[i];

@@ -235,6 +235,25 @@ const DenseVector* bare_leaf(const ExprNode& n) {
     return nullptr;
 }
 
+// A bare constant item (e.g. the Jacobian's 0 / 1 / gamma-1 entries): the
+// bits every element of a destination of precision `dest` holds once the
+// reference evaluates it -- the constant narrowed to its own precision
+// (narrow_value, proj/src/scalar_ops.hpp:81-85), then stored as `dest`.
+bool bare_constant(const ExprNode& n, Precision dest, uint64_t* bits) {
+    if (n.kind == NodeKind::Tagged || n.kind == NodeKind::Cached)
+        return bare_constant(*n.left, dest, bits);
+    if (n.kind != NodeKind::Constant) return false;
+    const double v = n.prec == Precision::f32 ? double(float(n.value)) : n.value;
+    *bits = 0;
+    if (dest == Precision::f32) {
+        const float f = float(v);
+        std::memcpy(bits, &f, sizeof f);
+    } else {
+        std::memcpy(bits, &v, sizeof v);
+    }
+    return true;
+}
+
 // One output of a plan: a host vector (staged), a device plane, or neither
 // (a NULL slot: the reduce-only wave-speed pass writes no plane).
 struct Out {
@@ -257,6 +276,18 @@ struct Plan {
     // the momentum fields), when that copy can be made host-side instead of
     // crossing PCIe twice; nullptr otherwise.  Set by block_impl.
     std::vector<const DenseVector*> pass_src;
+    // Per output: 1 when a bare constant item is filled host-side (bits in
+    // fill_bits) instead of shipped over PCIe.  Set by block_impl.
+    std::vector<char> has_fill;
+    std::vector<uint64_t> fill_bits;
+};
+
+// One host-side write: a copy of src, or (src == nullptr) a fill of every
+// element of dst with the bits `fill` of dst's precision.
+struct HostWrite {
+    DenseVector* dst;
+    const DenseVector* src;
+    uint64_t fill;
 };
 
 struct DeviceGuard {
@@ -289,25 +320,37 @@ HostCtx& host_ctx(int ordinal) {
     return *p;
 }
 
-// Host-side copies of pass-through items, on a few threads, running while
-// the device pipeline streams the computed items.  Joined on destruction.
+// Host-side copies of pass-through items and fills of constant items, on a
+// few threads, running while the device pipeline streams the computed
+// items.  Joined on destruction.
 struct HostCopies {
     std::vector<std::thread> threads;
-    explicit HostCopies(const std::vector<std::pair<DenseVector*, const DenseVector*>>& jobs) {
+    explicit HostCopies(const std::vector<HostWrite>& jobs) {
         if (jobs.empty()) return;
         std::size_t total = 0;
-        for (const auto& j : jobs) total += j.second->byte_size();
+        for (const auto& j : jobs) total += j.dst->byte_size();
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         const unsigned nt = std::min<unsigned>(4u, std::max(1u, hw / 4));
-        const std::size_t per = (total + nt - 1) / nt;
+        const std::size_t per = ((total + nt - 1) / nt + 63) & ~std::size_t(63);  // whole elements
         auto copy = [jobs](std::size_t lo, std::size_t hi) {
             std::size_t base = 0;
-            for (const auto& [dst, src] : jobs) {
-                const std::size_t b = src->byte_size();
+            for (const HostWrite& j : jobs) {
+                const std::size_t b = j.dst->byte_size();
                 const std::size_t a = std::max(lo, base), e = std::min(hi, base + b);
-                if (a < e)
-                    std::memcpy(static_cast<char*>(dst->raw()) + (a - base),
-                                static_cast<const char*>(src->raw()) + (a - base), e - a);
+                char* d = static_cast<char*>(j.dst->raw()) + (a - base);
+                if (a < e && j.src) {
+                    std::memcpy(d, static_cast<const char*>(j.src->raw()) + (a - base), e - a);
+                } else if (a < e && j.fill == 0) {
+                    std::memset(d, 0, e - a);
+                } else if (a < e && j.dst->precision() == Precision::f64) {
+                    double v;
+                    std::memcpy(&v, &j.fill, sizeof v);
+                    std::fill_n(reinterpret_cast<double*>(d), (e - a) / sizeof v, v);
+                } else if (a < e) {
+                    float v;
+                    std::memcpy(&v, &j.fill, sizeof v);
+                    std::fill_n(reinterpret_cast<float*>(d), (e - a) / sizeof v, v);
+                }
                 base += b;
             }
         };
@@ -359,7 +402,7 @@ double combine_max(const std::vector<double>& v, bool f64) {
 double run_sliced(const DeviceBackend& be, const Plan& plan, std::size_t n,
                   const std::vector<void*>& args, const std::vector<uint8_t>& prec,
                   const std::vector<uint8_t>& on_dev, bool reduce,
-                  const std::vector<std::pair<DenseVector*, const DenseVector*>>& pass) {
+                  const std::vector<HostWrite>& pass) {
     const std::size_t G = be.ordinals.size();
     std::vector<double> lam(G, 0.0);
     std::vector<fvb_status> st(G, FVB_OK);
@@ -414,13 +457,17 @@ void run(const DeviceBackend& be, Plan& plan, std::size_t n, void* red) {
     std::vector<void*> args(nout + nin, nullptr);
     std::vector<uint8_t> prec(nout + nin, 1), on_dev(nout + nin, 0);
     bool staged = false;
-    std::vector<std::pair<DenseVector*, const DenseVector*>> pass;
+    std::vector<HostWrite> pass;
     for (std::size_t j = 0; j < nout; ++j) {
         const Out& o = plan.outs[j];
         prec[j] = o.prec() == Precision::f64 ? 1 : 0;
         if (j < plan.pass_src.size() && plan.pass_src[j]) {
             on_dev[j] = 2;  // computed into device scratch only; copied host-side
-            pass.push_back({o.host, plan.pass_src[j]});
+            pass.push_back({o.host, plan.pass_src[j], 0});
+            staged = true;
+        } else if (j < plan.has_fill.size() && plan.has_fill[j]) {
+            on_dev[j] = 2;  // computed into device scratch only; filled host-side
+            pass.push_back({o.host, nullptr, plan.fill_bits[j]});
             staged = true;
         } else if (o.dev) {
             args[j] = o.dev->data();
@@ -778,10 +825,29 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
         // bare-leaf items of a fused block whose source and destination are
         // both host vectors of one precision, and whose source no item
         // overwrites: copied host-side while the device pipeline runs
+        // ... and bare constant items of host destinations are filled
+        // host-side (the Jacobian's 30 constant entries of 75 in 3-D)
         plan.pass_src.assign(plan.outs.size(), nullptr);
+        plan.has_fill.assign(plan.outs.size(), 0);
+        plan.fill_bits.assign(plan.outs.size(), 0);
+        // Host-side writes run concurrently with the device pipeline, so
+        // their destination must be no leaf of the block (the kernel may
+        // still be reading it) and no other item's destination.
+        auto exclusive = [&](const DenseVector* d) {
+            for (const DenseVector* l : plan.leaves)
+                if (l == d) return false;
+            std::size_t uses = 0;
+            for (const Out& w : plan.outs) uses += w.host == d;
+            return uses == 1;
+        };
         for (std::size_t j = 0; j < items.size(); ++j) {
-            const DenseVector* src = bare_leaf(items[j].node());
             const Out& o = plan.outs[j];
+            if (!o.host || !exclusive(o.host)) continue;
+            if (bare_constant(items[j].node(), o.host->precision(), &plan.fill_bits[j])) {
+                plan.has_fill[j] = 1;
+                continue;
+            }
+            const DenseVector* src = bare_leaf(items[j].node());
             if (!src || !o.host || o.host->precision() != src->precision() ||
                 (be.residency && be.residency->find(src)))
                 continue;

@@ -622,6 +622,40 @@ void run_gpu() {
         return "";
     });
 
+    check("host-side writes: constant items filled on the host, never over a plane the kernel reads", [&] {
+        // Bare constant items of host destinations are filled by host threads
+        // while the device pipeline streams the rest -- unless the
+        // destination is also a leaf of the block (here item 0 reads the
+        // plane item 1 overwrites with a constant: the reference reads the
+        // old values, block.cpp:413-451) or another item's destination.
+        const std::size_t n = 1'000'003;
+        dev::DeviceBackend small = be;
+        small.chunk_points = 1 << 16;  // many chunks: a racing fill would show
+        for (Precision P : {Precision::f64, Precision::f32}) {
+            SplitMix64 rng(5);
+            DenseVector a = testutil::make_vec(P, n, rng);
+            std::vector<DenseVector> w, g;
+            for (int i = 0; i < 3; ++i) {
+                w.emplace_back(P, n);
+                g.emplace_back(P, n);
+            }
+            BlockColVector want(std::move(w)), got(std::move(g));
+            for (BlockColVector* d : {&want, &got})
+                for (std::size_t i = 0; i < n; ++i) d->get(1).set(i, double(i % 7) - 3.0);
+            auto block = [&](BlockColVector& d) {
+                const Expr b = leaf(d.get(1));
+                return make_block_expr(3, 1, b * b + leaf(a), constant(2.5, b),
+                                       constant(0.1, Precision::f32));
+            };
+            evaluate_block(ref, block(want), want);
+            dev::evaluate_block(small, block(got), got);
+            for (std::size_t r = 0; r < 3; ++r)
+                if (!same_bits(want.get(r), got.get(r)))
+                    fail("item " + std::to_string(r) + " differs from the reference");
+        }
+        return "";
+    });
+
     check("narrowing rules on device: f32 constants, one rounding into a narrow store", [&] {
         // test_backend.cpp:122-138
         DenseVector ones(Precision::f32, 9000);

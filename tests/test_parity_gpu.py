@@ -336,7 +336,26 @@ def test_host_path_matches_device(cuda, orc, pinned):
     _, lam = ctx.jacobian(hs, dim, jo)
     j_np, lam_np = orc.jacobian(dim, s_np)
     assert lam == lam_np
-    assert all_same([t.numpy() for t in jo[:25]], j_np[:25])
+    # all 75, the 30 constant entries filled host-side included
+    assert all_same([t.numpy() for t in jo], j_np)
+    ctx.close()
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_host_jacobian_constant_fills(cuda, orc, prec):
+    # the constant entries (0, 1, gamma-1) are filled by host threads: every
+    # dimension, both precisions, a non-default gas (another gamma-1), and
+    # outputs pre-filled with garbage so a skipped fill would show
+    g, og = fvb.Gas(5, 2, 3, 2), orc.gas(cp=(5, 2), cv=(3, 2))
+    ctx = fvb.HostContext(0, chunk_points=1 << 12)
+    for dim in (1, 2, 3):
+        s_np = orc.random_state(dim, 20_011, seed=31 + dim, prec=prec)
+        hs = [torch.from_numpy(a) for a in s_np]
+        jo = [torch.full((20_011,), float("nan"), dtype=DT[prec]) for _ in range(dim * (dim + 2) ** 2)]
+        _, lam = ctx.jacobian(hs, dim, jo, gas=g)
+        j_np, lam_np = orc.jacobian(dim, s_np, gas=og)
+        assert lam == lam_np
+        assert all_same([t.numpy() for t in jo], j_np), dim
     ctx.close()
 
 
