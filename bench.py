@@ -46,6 +46,11 @@ CONFIGS = {
     "axpy": (0, 2, 1, 1_000_000, "C1: UETLI y = 0.5*sin(x+y)"),
     "vmag2": (3, 4, 1, 100_000_000,
               "paper micro-benchmark (mx^2+my^2+mz^2)/rho^2 = derived_v_mag2, 3D"),
+    # the remaining entry points of SURVEY §8a, same N (not BASELINE configs)
+    "prim2cons3d": (3, 5, 4, 100_000_000, "3D prim->cons: m = rho*v, rhoE (rho passed through)"),
+    "flux_prim3d": (3, 5, 15, 100_000_000, "3D inviscid fluxes of a primitive state"),
+    "eos": (0, 2, 2, 100_000_000, "ideal-gas EOS p(rho, e), T(rho, e)"),
+    "cfl3d": (3, 5, 0, 100_000_000, "3D standalone CFL max wave speed (reduction only)"),
 }
 
 
@@ -170,7 +175,8 @@ class ClockSampler:
 
 # ---- the reference arm (CPU) -----------------------------------------------------------
 
-REF_WHICH = {"flux3d": 0, "cons2prim1d": 1, "jacobian3d": 2, "axpy": 3, "vmag2": 4}
+REF_WHICH = {"flux3d": 0, "cons2prim1d": 1, "jacobian3d": 2, "axpy": 3, "vmag2": 4,
+             "prim2cons3d": 5, "flux_prim3d": 6, "eos": 7, "cfl3d": 8}
 
 
 def reference_run(cfg_name, prec, steps, warmup, sample, threads):
@@ -270,7 +276,8 @@ def end_to_end(a, fvb, ins, n, n_in, n_out, dim, dt, esize, local, dist, world, 
 
 
 # configs whose e2e runs the registry kernel through fvb_launch_host
-LAUNCH_HOST_PATTERN = {"cons2prim1d": "cons2prim_c1", "vmag2": "v_mag23"}
+LAUNCH_HOST_PATTERN = {"cons2prim1d": "cons2prim_c1", "vmag2": "v_mag23",
+                       "prim2cons3d": "prim2cons3", "flux_prim3d": "flux_prim3"}
 # the default gas's named constants (EosSpec(): gamma = 7/5, R = 1, cv = 5/2)
 _GAS_CONSTS = {"half": 0.5, "gm1": 0.4, "gamma": 1.4, "zero": 0.0, "one": 1.0, "cv": 2.5}
 
@@ -321,6 +328,10 @@ def device_run(a, rank, world, local):
             y = fvb.synth_uniform(n, prec=prec, seed=1, first=world * n + first)
             ins = [x, y]
             outs = [y]
+        elif a.config == "eos":  # rho and rho*E of the random state, as rho and e
+            st = fvb.synth_state(1, n, prec=prec, seed=0x5EED, first=first)
+            ins = [st[0], st[2]]
+            outs = [torch.empty(n, dtype=dt, device=dev) for _ in range(2)]
         else:
             ins = fvb.synth_state(dim, n, prec=prec, seed=0x5EED, first=first)
             outs = [torch.empty(n, dtype=dt, device=dev) for _ in range(n_out)]
@@ -336,6 +347,14 @@ def device_run(a, rank, world, local):
             fvb.jacobian(ins, dim, out=outs, lambda_max=lam, stream=stream)
         elif a.config == "vmag2":
             fvb.v_mag2(ins, dim, out=outs[0], stream=stream)
+        elif a.config == "prim2cons3d":  # the state's planes read as [rho, v, p]
+            fvb.prim2cons(ins, dim, out=outs, stream=stream)
+        elif a.config == "flux_prim3d":
+            fvb.flux_prim(ins, dim, out=outs, stream=stream)
+        elif a.config == "eos":
+            fvb.eos(ins[0], ins[1], p=outs[0], T=outs[1], stream=stream)
+        elif a.config == "cfl3d":
+            fvb.wave_speed_max(ins, dim, lambda_max=lam, stream=stream)
         else:
             fvb.axpy_sin(ins[0], ins[1], stream=stream)
 
@@ -420,7 +439,7 @@ def device_run(a, rank, world, local):
 
     # ---- end to end through the host-buffer C-ABI call -----------------------------
     e2e = None
-    if not a.no_e2e and a.config != "axpy":
+    if not a.no_e2e and a.config not in ("axpy", "eos", "cfl3d"):
         try:
             e2e = end_to_end(a, fvb, ins, n, n_in, n_out, dim, dt, esize, local, dist, world,
                              dev, torch)

@@ -331,6 +331,9 @@ int fvr_wave_speed(const long long* gas, int dim, int prec, std::uint64_t n,
 //   1 = cons->prim fields + sound speed, one evaluate per field (C2)
 //   2 = Jacobian evaluate_block + evaluate(lambda) + host max   (C4)
 //   3 = axpy-sin y = 0.5*sin(x+y), in place                     (C1)
+//   4 = derived_v_mag2 (the paper's micro-benchmark)
+//   5 = prim->cons fields, 6 = primitive-formulation flux,
+//   7 = EOS p and T, 8 = standalone CFL lambda + host max
 // Writes per-rep nanoseconds into times_ns[0..reps).
 // ---------------------------------------------------------------------------
 int fvr_time_config(int which, int dim, int prec, std::uint64_t n, int workers, int reps,
@@ -388,6 +391,49 @@ int fvr_time_config(int which, int dim, int prec, std::uint64_t n, int workers, 
             DenseVector out(P, n);
             evaluate(be, vm, out);
             for (int r = 0; r < reps; ++r) times_ns[r] = time_ns([&] { evaluate(be, vm, out); });
+        } else if (which == 5 || which == 6) {
+            // the same planes read as a primitive state [rho, v..., p]:
+            // 5 = convert(prim, Conservative), one evaluate per computed field
+            // 6 = the primitive-formulation flux (fluid.cpp:290-298)
+            StateSet pr = state_primitive(EosSpec(), d, leaves(f));
+            if (which == 5) {
+                StateSet cons = convert(pr, Formulation::Conservative);
+                std::vector<DenseVector> out(d + 1, DenseVector(P, n));
+                auto run = [&] {
+                    for (std::size_t j = 0; j < d + 1; ++j) evaluate(be, cons.field(j + 1), out[j]);
+                };
+                run();
+                for (int r = 0; r < reps; ++r) times_ns[r] = time_ns(run);
+            } else {
+                BlockExpr flux = inviscid_flux(pr);
+                BlockVectorGrid grid(w, d, P, n);
+                evaluate_block(be, flux, grid);
+                for (int r = 0; r < reps; ++r)
+                    times_ns[r] = time_ns([&] { evaluate_block(be, flux, grid); });
+            }
+        } else if (which == 7) {
+            // the ideal-gas EOS closures p(rho, e) and T(rho, e) (fluid.cpp:57-65)
+            const Expr rho = leaf(f[0]), e = leaf(f[d + 1]);
+            Expr pe = eos_ideal_p(rho, e, EosSpec()), te = eos_ideal_T(rho, e, EosSpec());
+            DenseVector p(P, n), T(P, n);
+            auto run = [&] {
+                evaluate(be, pe, p);
+                evaluate(be, te, T);
+            };
+            run();
+            for (int r = 0; r < reps; ++r) times_ns[r] = time_ns(run);
+        } else if (which == 8) {
+            // standalone CFL: evaluate(lambda) + host max
+            Expr lam_e = wave_speed(u);
+            DenseVector lam(P, n);
+            volatile double sink = 0;
+            auto run = [&] {
+                evaluate(be, lam_e, lam);
+                sink = host_max(lam);
+            };
+            run();
+            for (int r = 0; r < reps; ++r) times_ns[r] = time_ns(run);
+            (void)sink;
         } else {
             throw Error("unknown timing config");
         }

@@ -50,12 +50,12 @@ fvb_status fvb_wave_speed_max(const fvb_gas* gas, uint32_t dim, uint8_t prec, ui
         if (fvb_status st = reset_scalar<double>(lambda_max, s)) return st;
         auto red = static_cast<unsigned long long*>(lambda_max);
         if (lambda) return run_dim<WaveSpeed1, true, false, double>(dim, in, outs, n, gas, red, s);
-        return run_dim<WaveSpeed0, true, false, double>(dim, in, outs, n, gas, red, s);
+        return run_dim<WaveSpeed0, true, true, double>(dim, in, outs, n, gas, red, s);
     }
     if (fvb_status st = reset_scalar<float>(lambda_max, s)) return st;
     auto red = static_cast<unsigned int*>(lambda_max);
     if (lambda) return run_dim<WaveSpeed1, true, false, float>(dim, in, outs, n, gas, red, s);
-    return run_dim<WaveSpeed0, true, false, float>(dim, in, outs, n, gas, red, s);
+    return run_dim<WaveSpeed0, true, true, float>(dim, in, outs, n, gas, red, s);
 }
 
 }  // extern "C"
