@@ -174,6 +174,16 @@ FVB_API fvb_status fvb_csr_matvec_acc(uint8_t prec_y, uint8_t prec_x, uint64_t r
                                       const double* values, const void* x, void* y,
                                       void* stream);
 
+/* The same with 32-bit column indices (any matrix with fewer than 2^32
+ * columns): the device-resident layout the C++ adapter's DeviceCsr keeps,
+ * 12 instead of 16 bytes per nonzero of index + value stream.  The
+ * reference stores size_t indices (SparseMatrix, block.hpp:42-44); the
+ * narrowing happens once, at upload, and changes no result bit. */
+FVB_API fvb_status fvb_csr_matvec_acc_u32(uint8_t prec_y, uint8_t prec_x, uint64_t rows,
+                                          uint64_t nnz, const uint64_t* row_ptr,
+                                          const uint32_t* col_idx, const double* values,
+                                          const void* x, void* y, void* stream);
+
 /* On-device synthetic inputs, bit-identical to the reference's host
  * generators because SplitMix64 is random-access (proj/include/fusevec/
  * rng.hpp:8-28):

@@ -30,6 +30,7 @@ EXPORTED = (
     "fvb_jacobian",
     "fvb_wave_speed_max",
     "fvb_csr_matvec_acc",
+    "fvb_csr_matvec_acc_u32",
     "fvb_synth_state",
     "fvb_synth_uniform",
     "fvb_lookup",
@@ -153,6 +154,7 @@ def _declare(L):
         "fvb_jacobian": (i32, [gas, u32, u8, u64, pp, pp, vp, vp]),
         "fvb_wave_speed_max": (i32, [gas, u32, u8, u64, pp, vp, vp, vp]),
         "fvb_csr_matvec_acc": (i32, [u8, u8, u64, u64, vp, vp, vp, vp, vp, vp]),
+        "fvb_csr_matvec_acc_u32": (i32, [u8, u8, u64, u64, vp, vp, vp, vp, vp, vp]),
         "fvb_synth_state": (i32, [u32, u8, u64, u64, u64, pp, vp]),
         "fvb_synth_uniform": (i32, [u8, u64, u64, u64, ctypes.c_double, ctypes.c_double, vp,
                                     vp]),

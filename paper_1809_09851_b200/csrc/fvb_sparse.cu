@@ -35,9 +35,9 @@ constexpr int kTile = 256;  // products staged per warp per round
 
 // Row per thread, nonzeros walked in stored order (the simple form; kept for
 // the comparison in tools/csr_bench.py via FVB_CSR_MODE=row).
-template <class TY, class TX>
+template <class TY, class TX, class IT>
 __global__ void __launch_bounds__(kCsrThreads)
-    csr_row_kernel(uint64_t rows, const uint64_t* __restrict__ rp, const uint64_t* __restrict__ ci,
+    csr_row_kernel(uint64_t rows, const uint64_t* __restrict__ rp, const IT* __restrict__ ci,
                    const double* __restrict__ v, const TX* __restrict__ x, TY* __restrict__ y) {
     const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < rows; r += stride) {
@@ -50,10 +50,10 @@ __global__ void __launch_bounds__(kCsrThreads)
 }
 
 // Warp-staged: see the file comment.  One warp per 32 rows, grid-stride.
-template <class TY, class TX, int MINB, int UNR>
+template <class TY, class TX, class IT, int MINB, int UNR>
 __global__ void __launch_bounds__(kCsrThreads, MINB)
     csr_warp_kernel(uint64_t rows, const uint64_t* __restrict__ rp,
-                    const uint64_t* __restrict__ ci, const double* __restrict__ v,
+                    const IT* __restrict__ ci, const double* __restrict__ v,
                     const TX* __restrict__ x, TY* __restrict__ y) {
     __shared__ TY prod[kCsrThreads / 32][kTile];
     const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kCsrThreads, MINB)
         for (uint64_t base = B; base < E; base += kTile) {
             const unsigned lim = E - base < uint64_t(kTile) ? unsigned(E - base) : unsigned(kTile);
             const double* vb = v + base;
-            const uint64_t* cb = ci + base;
+            const IT* cb = ci + base;
 #pragma unroll UNR
             for (unsigned t = lane; t < lim; t += 32)
                 p[t] = static_cast<TY>(vb[t]) * static_cast<TY>(x[cb[t]]);
@@ -97,11 +97,11 @@ bool rowwise() {
     return e && *e && *e != '0';
 }
 
-template <class TY, class TX>
-fvb_status launch_csr(uint64_t rows, const uint64_t* rp, const uint64_t* ci, const double* v,
+template <class TY, class TX, class IT>
+fvb_status launch_csr(uint64_t rows, const uint64_t* rp, const IT* ci, const double* v,
                       const void* x, void* y, cudaStream_t s) {
     if (rowwise()) {
-        csr_row_kernel<TY, TX><<<simple_grid(rows), kCsrThreads, 0, s>>>(
+        csr_row_kernel<TY, TX, IT><<<simple_grid(rows), kCsrThreads, 0, s>>>(
             rows, rp, ci, v, static_cast<const TX*>(x), static_cast<TY*>(y));
     } else {
         // one pass over the rows: a warp per 32 rows, capped at a few waves
@@ -112,12 +112,35 @@ fvb_status launch_csr(uint64_t rows, const uint64_t* rp, const uint64_t* ci, con
         const unsigned g = unsigned(grid ? grid : 1);
         const TX* xx = static_cast<const TX*>(x);
         TY* yy = static_cast<TY*>(y);
-        // 8 resident CTAs (32 registers) and two tile entries in flight per
-        // lane: the measured best (profiles/r01_csr_shapes.txt)
-        csr_warp_kernel<TY, TX, 8, 2><<<g, kCsrThreads, 0, s>>>(rows, rp, ci, v, xx, yy);
+        // 8 resident CTAs (32 registers) and three tile entries in flight
+        // per lane: the measured best (profiles/r01_csr_shapes.txt)
+        const char* u = std::getenv("FVB_CSR_UNROLL");  // sweep knob: 2, 3 (default), 4
+        if (u && !std::strcmp(u, "4"))
+            csr_warp_kernel<TY, TX, IT, 8, 4><<<g, kCsrThreads, 0, s>>>(rows, rp, ci, v, xx, yy);
+        else if (u && !std::strcmp(u, "2"))
+            csr_warp_kernel<TY, TX, IT, 8, 2><<<g, kCsrThreads, 0, s>>>(rows, rp, ci, v, xx, yy);
+        else
+            csr_warp_kernel<TY, TX, IT, 8, 3><<<g, kCsrThreads, 0, s>>>(rows, rp, ci, v, xx, yy);
     }
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? FVB_OK : cuda_fail(e, "csr matvec launch");
+}
+
+template <class IT>
+fvb_status csr_entry(uint8_t prec_y, uint8_t prec_x, uint64_t rows, uint64_t nnz,
+                     const uint64_t* row_ptr, const IT* col_idx, const double* values,
+                     const void* x, void* y, void* stream) {
+    if (prec_y > 1 || prec_x > 1) return fail(FVB_EPREC, "precision code must be 0 or 1");
+    if (rows == 0) return FVB_OK;
+    if (!row_ptr || !y || (nnz && (!col_idx || !values || !x)))
+        return fail(FVB_EARG, "NULL CSR array or plane");
+    auto s = static_cast<cudaStream_t>(stream);
+    if (prec_y == FVB_F64)
+        return prec_x == FVB_F64
+                   ? launch_csr<double, double, IT>(rows, row_ptr, col_idx, values, x, y, s)
+                   : launch_csr<double, float, IT>(rows, row_ptr, col_idx, values, x, y, s);
+    return prec_x == FVB_F64 ? launch_csr<float, double, IT>(rows, row_ptr, col_idx, values, x, y, s)
+                             : launch_csr<float, float, IT>(rows, row_ptr, col_idx, values, x, y, s);
 }
 
 }  // namespace
@@ -130,16 +153,13 @@ extern "C" {
 fvb_status fvb_csr_matvec_acc(uint8_t prec_y, uint8_t prec_x, uint64_t rows, uint64_t nnz,
                               const uint64_t* row_ptr, const uint64_t* col_idx,
                               const double* values, const void* x, void* y, void* stream) {
-    if (prec_y > 1 || prec_x > 1) return fail(FVB_EPREC, "precision code must be 0 or 1");
-    if (rows == 0) return FVB_OK;
-    if (!row_ptr || !y || (nnz && (!col_idx || !values || !x)))
-        return fail(FVB_EARG, "NULL CSR array or plane");
-    auto s = static_cast<cudaStream_t>(stream);
-    if (prec_y == FVB_F64)
-        return prec_x == FVB_F64 ? launch_csr<double, double>(rows, row_ptr, col_idx, values, x, y, s)
-                                 : launch_csr<double, float>(rows, row_ptr, col_idx, values, x, y, s);
-    return prec_x == FVB_F64 ? launch_csr<float, double>(rows, row_ptr, col_idx, values, x, y, s)
-                             : launch_csr<float, float>(rows, row_ptr, col_idx, values, x, y, s);
+    return csr_entry(prec_y, prec_x, rows, nnz, row_ptr, col_idx, values, x, y, stream);
+}
+
+fvb_status fvb_csr_matvec_acc_u32(uint8_t prec_y, uint8_t prec_x, uint64_t rows, uint64_t nnz,
+                                  const uint64_t* row_ptr, const uint32_t* col_idx,
+                                  const double* values, const void* x, void* y, void* stream) {
+    return csr_entry(prec_y, prec_x, rows, nnz, row_ptr, col_idx, values, x, y, stream);
 }
 
 }  // extern "C"

@@ -207,13 +207,15 @@ def wave_speed_max(state, dim, lam_out=None, lambda_max=None, gas=None, stream=N
 
 
 def csr_matvec_acc(row_ptr, col_idx, values, x, y, stream=None):
-    """y += A x for a CSR matrix (block.cpp:345-356): row_ptr (rows+1) and
-    col_idx (nnz) int64 CUDA tensors holding the unsigned indices, values
-    float64 (already narrowed to the matrix precision); x and y f32/f64
-    planes.  Each row is summed in stored order in y's precision."""
-    for t, what in ((row_ptr, "row_ptr"), (col_idx, "col_idx")):
-        if not t.is_cuda or t.dtype != torch.int64 or t.dim() != 1:
-            raise N.ArgumentError(N.FVB_EARG, f"{what} must be a 1-D int64 CUDA tensor")
+    """y += A x for a CSR matrix (block.cpp:345-356): row_ptr (rows+1) int64
+    and col_idx (nnz) int64 -- or int32, the narrow device layout
+    (fvb_csr_matvec_acc_u32) -- CUDA tensors holding the unsigned indices,
+    values float64 (already narrowed to the matrix precision); x and y
+    f32/f64 planes.  Each row is summed in stored order in y's precision."""
+    if not row_ptr.is_cuda or row_ptr.dtype != torch.int64 or row_ptr.dim() != 1:
+        raise N.ArgumentError(N.FVB_EARG, "row_ptr must be a 1-D int64 CUDA tensor")
+    if not col_idx.is_cuda or col_idx.dtype not in (torch.int64, torch.int32) or col_idx.dim() != 1:
+        raise N.ArgumentError(N.FVB_EARG, "col_idx must be a 1-D int64 or int32 CUDA tensor")
     if not values.is_cuda or values.dtype != torch.float64 or values.numel() != col_idx.numel():
         raise N.ArgumentError(N.FVB_EARG, "values must be float64 with one entry per index")
     (xp,), cols, px = _planes([x], "x")
@@ -221,9 +223,10 @@ def csr_matvec_acc(row_ptr, col_idx, values, x, y, stream=None):
     if row_ptr.numel() != rows + 1:
         raise N.LengthMismatch(N.FVB_ELEN, f"row_ptr has {row_ptr.numel()} entries for "
                                            f"{rows} rows")
-    N.check(N.lib().fvb_csr_matvec_acc(py, px, rows, col_idx.numel(), row_ptr.data_ptr(),
-                                       col_idx.data_ptr(), values.data_ptr(), xp, yp,
-                                       _stream(stream)))
+    fn = N.lib().fvb_csr_matvec_acc_u32 if col_idx.dtype == torch.int32 else \
+        N.lib().fvb_csr_matvec_acc
+    N.check(fn(py, px, rows, col_idx.numel(), row_ptr.data_ptr(), col_idx.data_ptr(),
+               values.data_ptr(), xp, yp, _stream(stream)))
     return y
 
 

@@ -630,8 +630,14 @@ void run_matvec(const DeviceBackend& be, std::vector<std::pair<const BlockItem*,
             const int px = x.precision() == Precision::f64 ? 1 : 0;
             if (const DeviceCsr* dm = be.residency ? be.residency->find(t.mat) : nullptr) {
                 // a resident matrix: no upload
-                fvb_check(fvb_csr_matvec_acc(py, px, rows, dm->nnz(), dm->row_ptr(),
-                                             dm->col_idx(), dm->values(), x.data(), y->data(), s));
+                if (dm->narrow_indices())
+                    fvb_check(fvb_csr_matvec_acc_u32(py, px, rows, dm->nnz(), dm->row_ptr(),
+                                                     dm->col_idx32(), dm->values(), x.data(),
+                                                     y->data(), s));
+                else
+                    fvb_check(fvb_csr_matvec_acc(py, px, rows, dm->nnz(), dm->row_ptr(),
+                                                 dm->col_idx(), dm->values(), x.data(), y->data(),
+                                                 s));
                 continue;
             }
             const auto& rp = t.mat->row_ptr();
@@ -1000,24 +1006,34 @@ DeviceCsr::~DeviceCsr() {
 void DeviceCsr::upload(const SparseMatrix& m) {
     static_assert(sizeof(std::size_t) == sizeof(std::uint64_t), "64-bit size_t");
     DeviceGuard guard(ordinal_);
-    if (m.rows() != rows_ || m.nnz() != nnz_ || !rp_) {
+    const bool narrow = m.cols() <= std::size_t(UINT32_MAX);
+    if (m.rows() != rows_ || m.nnz() != nnz_ || narrow != narrow_ || !rp_) {
         if (rp_) cudaFree(rp_);
         if (ci_) cudaFree(ci_);
         if (v_) cudaFree(v_);
-        rp_ = ci_ = nullptr;
+        rp_ = nullptr;
+        ci_ = nullptr;
         v_ = nullptr;
         cuda_check(cudaMalloc(&rp_, (m.rows() + 1) * 8), "csr allocation");
         if (m.nnz()) {
-            cuda_check(cudaMalloc(&ci_, m.nnz() * 8), "csr allocation");
+            cuda_check(cudaMalloc(&ci_, m.nnz() * (narrow ? 4 : 8)), "csr allocation");
             cuda_check(cudaMalloc(&v_, m.nnz() * 8), "csr allocation");
         }
     }
     rows_ = m.rows();
     cols_ = m.cols();
     nnz_ = m.nnz();
+    narrow_ = narrow;
     cuda_check(cudaMemcpy(rp_, m.row_ptr().data(), (rows_ + 1) * 8, cudaMemcpyHostToDevice),
                "csr upload");
-    if (nnz_) {
+    if (nnz_ && narrow_) {
+        // the once-per-upload narrowing: every index < cols <= 2^32 - 1
+        const std::vector<std::size_t>& ci = m.col_idx();
+        std::vector<std::uint32_t> ci32(ci.begin(), ci.end());
+        cuda_check(cudaMemcpy(ci_, ci32.data(), nnz_ * 4, cudaMemcpyHostToDevice), "csr upload");
+        cuda_check(cudaMemcpy(v_, m.values().data(), nnz_ * 8, cudaMemcpyHostToDevice),
+                   "csr upload");
+    } else if (nnz_) {
         cuda_check(cudaMemcpy(ci_, m.col_idx().data(), nnz_ * 8, cudaMemcpyHostToDevice),
                    "csr upload");
         cuda_check(cudaMemcpy(v_, m.values().data(), nnz_ * 8, cudaMemcpyHostToDevice),

@@ -92,7 +92,10 @@ DeviceVector make_temp(Precision prec, std::size_t len);
 /// A SparseMatrix's CSR arrays uploaded once (row pointers, column indices
 /// and the stored values, block.hpp:42-44), for repeated block matvecs
 /// without re-sending the matrix over PCIe.  A snapshot: re-upload after
-/// SparseMatrix::set_value.
+/// SparseMatrix::set_value.  Column indices are kept as 32-bit integers
+/// when the matrix has fewer than 2^32 columns (12 instead of 16 streamed
+/// bytes per nonzero; no result bit changes), else as the reference's
+/// 64-bit size_t.
 class DeviceCsr {
   public:
     explicit DeviceCsr(const SparseMatrix& m, int ordinal = 0);
@@ -105,14 +108,18 @@ class DeviceCsr {
     std::size_t cols() const { return cols_; }
     std::size_t nnz() const { return nnz_; }
     const std::uint64_t* row_ptr() const { return rp_; }
-    const std::uint64_t* col_idx() const { return ci_; }
+    /// true: col_idx32() holds the indices; false: col_idx() does
+    bool narrow_indices() const { return narrow_; }
+    const std::uint64_t* col_idx() const { return narrow_ ? nullptr : static_cast<const std::uint64_t*>(ci_); }
+    const std::uint32_t* col_idx32() const { return narrow_ ? static_cast<const std::uint32_t*>(ci_) : nullptr; }
     const double* values() const { return v_; }
 
   private:
     int ordinal_ = 0;
     std::size_t rows_ = 0, cols_ = 0, nnz_ = 0;
+    bool narrow_ = false;
     std::uint64_t* rp_ = nullptr;
-    std::uint64_t* ci_ = nullptr;
+    void* ci_ = nullptr;
     double* v_ = nullptr;
 };
 

@@ -150,8 +150,9 @@ def test_structural_key_kernels_stay_in_bounds(cuda, orc):
     A.check("structural-key kernels")
 
 
+@pytest.mark.parametrize("idx", ["u64", "u32"])
 @pytest.mark.parametrize("mode", ["row", "warp"])
-def test_csr_matvec_stays_in_bounds(cuda, mode, monkeypatch):
+def test_csr_matvec_stays_in_bounds(cuda, mode, idx, monkeypatch):
     monkeypatch.setenv("FVB_CSR_MODE", mode)
     A = Arena(cuda)
     rows, cols = 257, 301
@@ -167,16 +168,20 @@ def test_csr_matvec_stays_in_bounds(cuda, mode, monkeypatch):
     # values and indices in guarded planes too, one element off a 16-byte
     # boundary, checked unchanged after
     dv = A.inputs_from([np.array(vv)], 1)[0]
-    dci = A.plane(len(ci), 1, 3)
-    dci.view(torch.int64).copy_(torch.from_numpy(np.array(ci, np.uint64).view(np.int64)))
+    if idx == "u64":
+        dci = A.plane(len(ci), 1, 3)
+        dci.view(torch.int64).copy_(torch.from_numpy(np.array(ci, np.uint64).view(np.int64)))
+    else:  # 32-bit indices, 4 bytes off a 16-byte boundary
+        dci = A.plane(len(ci), 0, 1)
+        dci.view(torch.int32).copy_(torch.from_numpy(np.array(ci, np.int32)))
     A.inputs.append((dci, dci.clone()))
+    fn = N.lib().fvb_csr_matvec_acc if idx == "u64" else N.lib().fvb_csr_matvec_acc_u32
     xh = rng.uniform(-1, 1, cols)
     x = A.inputs_from([xh], 1)[0]
     y = A.plane(rows, 1, 3)
     y.zero_()
-    N.check(N.lib().fvb_csr_matvec_acc(1, 1, rows, len(ci), drp.data_ptr(), dci.data_ptr(),
-                                       dv.data_ptr(), x.data_ptr(), y.data_ptr(),
-                                       torch.cuda.current_stream().cuda_stream))
+    N.check(fn(1, 1, rows, len(ci), drp.data_ptr(), dci.data_ptr(), dv.data_ptr(), x.data_ptr(),
+               y.data_ptr(), torch.cuda.current_stream().cuda_stream))
     # csr_matvec_acc_t (proj/src/block.cpp:345-356): acc in stored order, y += acc
     want = np.zeros(rows)
     for r in range(rows):

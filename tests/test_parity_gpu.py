@@ -630,9 +630,10 @@ def csr_mode(request, monkeypatch):
     return request.param
 
 
+@pytest.mark.parametrize("idx", ["u64", "u32"])
 @pytest.mark.parametrize("y_prec,x_prec", [("f64", "f64"), ("f64", "f32"), ("f32", "f64"),
                                            ("f32", "f32")])
-def test_csr_matvec_bitwise(cuda, orc, y_prec, x_prec, csr_mode):
+def test_csr_matvec_bitwise(cuda, orc, y_prec, x_prec, csr_mode, idx):
     # Every CSR form against the oracle (pinned to the reference in
     # test_oracle.py): rows longer than one staging tile, warps whose range
     # spans several tiles, empty rows,
@@ -651,6 +652,8 @@ def test_csr_matvec_bitwise(cuda, orc, y_prec, x_prec, csr_mode):
         y0 = rng.uniform(-1, 1, rows).astype(yt[y_prec])
         want = orc.csr_matvec_acc(rp, ci, v, x, y0)
         drp, dci, dv = _csr_to_dev(rp, ci, v, cuda)
+        if idx == "u32":  # the narrow device layout (fvb_csr_matvec_acc_u32)
+            dci = dci.to(torch.int32)
         dx = torch.from_numpy(x).to(cuda)
         dy = torch.from_numpy(y0.copy()).to(cuda)
         fvb.csr_matvec_acc(drp, dci, dv, dx, dy)

@@ -44,35 +44,12 @@ def main():
     x = rng.uniform(-1, 1, rows)
     y0 = np.zeros(rows)
     drp = torch.from_numpy(rp.view(np.int64)).to(dev)
-    dci = torch.from_numpy(ci.view(np.int64)).to(dev)
+    dci64 = torch.from_numpy(ci.view(np.int64)).to(dev)
     dv = torch.from_numpy(v).to(dev)
     dx = torch.from_numpy(x).to(dev)
     dy = torch.zeros(rows, dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
-
-    def launch():
-        N.check(N.lib().fvb_csr_matvec_acc(1, 1, rows, nnz, drp.data_ptr(), dci.data_ptr(),
-                                           dv.data_ptr(), dx.data_ptr(), dy.data_ptr(),
-                                           stream.cuda_stream))
-
-    launch()
-    torch.cuda.synchronize()
     want = oracle.oracle().csr_matvec_acc(rp, ci, v, x, y0)
-    bitwise = dy.cpu().numpy().tobytes() == want.tobytes()
-    for _ in range(3):
-        launch()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2 between reps
-    times = []
-    for _ in range(a.reps):
-        flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        launch()
-        e1.record()
-        torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1) * 1e-3)
-    t = float(np.median(times))
-    bytes_ = 8 * (rows + 1) + 16 * nnz + 8 * rows + 16 * rows
     peak = 6548.2
     try:
         peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
@@ -80,11 +57,38 @@ def main():
         pass
     variant = os.environ.get("FVB_CSR_MODE", "") or (
         "rowwise" if os.environ.get("FVB_CSR_ROWWISE", "0") not in ("", "0") else "auto")
-    line = {"kernel": f"csr_{variant}", "grid": f"{a.n}^3", "rows": rows, "nnz": nnz,
-            "ms": t * 1e3, "grows_per_s": rows / t / 1e9, "algorithmic_bytes": bytes_,
-            "GBps": bytes_ / t / 1e9, "peak_GBps": peak, "frac": bytes_ / t / 1e9 / peak,
-            "bitwise_vs_oracle": bitwise, "l2": "flushed between reps"}
-    print(json.dumps(line), flush=True)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2 between reps
+    # the reference's 64-bit size_t indices, then the 32-bit device layout
+    # DeviceCsr keeps (fvb_csr_matvec_acc_u32): 16 vs 12 bytes per nonzero
+    for width, dci, fn in ((8, dci64, N.lib().fvb_csr_matvec_acc),
+                           (4, dci64.to(torch.int32), N.lib().fvb_csr_matvec_acc_u32)):
+        def launch():
+            N.check(fn(1, 1, rows, nnz, drp.data_ptr(), dci.data_ptr(), dv.data_ptr(),
+                       dx.data_ptr(), dy.data_ptr(), stream.cuda_stream))
+
+        dy.zero_()
+        launch()
+        torch.cuda.synchronize()
+        bitwise = dy.cpu().numpy().tobytes() == want.tobytes()
+        for _ in range(3):
+            launch()
+        times = []
+        for _ in range(a.reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            launch()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) * 1e-3)
+        t = float(np.median(times))
+        bytes_ = 8 * (rows + 1) + (8 + width) * nnz + 8 * rows + 16 * rows
+        line = {"kernel": f"csr_{variant}" + ("" if width == 8 else "_u32"), "grid": f"{a.n}^3",
+                "rows": rows, "nnz": nnz, "index_bytes": width,
+                "ms": t * 1e3, "grows_per_s": rows / t / 1e9, "algorithmic_bytes": bytes_,
+                "GBps": bytes_ / t / 1e9, "peak_GBps": peak, "frac": bytes_ / t / 1e9 / peak,
+                "bitwise_vs_oracle": bitwise, "l2": "flushed between reps"}
+        print(json.dumps(line), flush=True)
     ref = oracle.reference()
     if ref is not None and variant == "auto" and a.ref_n > 0:
         ts, rnnz = ref.time_csr(a.ref_n, 5)

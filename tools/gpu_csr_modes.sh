@@ -7,3 +7,6 @@ rm -f gpurun_out/csr_modes.jsonl
 for m in row warp; do
   FVB_CSR_MODE=$m timeout 300 python tools/csr_bench.py --n 256 --reps 20 --ref-n 0 >> gpurun_out/csr_modes.jsonl 2>> gpurun_out/csr_modes.err
 done
+for u in 2 4; do
+  FVB_CSR_MODE=warp FVB_CSR_UNROLL=$u timeout 300 python tools/csr_bench.py --n 256 --reps 20 --ref-n 0 | sed "s/\"kernel\": \"csr_warp/\"kernel\": \"csr_warp_unroll$u/" >> gpurun_out/csr_modes.jsonl 2>> gpurun_out/csr_modes.err
+done
