@@ -90,3 +90,39 @@ def test_random_cases_bitwise(cuda, orc, chunk):
             _, lam_np = orc.jacobian(dim, s_np, gas=og)
             torch.cuda.synchronize()
             assert lam.item() == float(lam_np) == lam_pts.max().item(), what
+
+
+@pytest.mark.parametrize("chunk", range(2))
+def test_random_host_buffer_cases_bitwise(cuda, orc, chunk):
+    # The host-buffer (end-to-end) path: random dimension, precision, gas,
+    # length, staging chunk (so chunks end anywhere: ragged last chunks,
+    # one-chunk ranges), pinned or pageable planes; the flux's host-side
+    # row-0 copies and the Jacobian's host-side constant fills included.
+    # Outputs start as NaN so a skipped host-side write shows.
+    rng = np.random.default_rng(2000 + chunk)
+    for case in range(20):
+        block = rng.choice(["flux", "jacobian"])
+        dim = int(rng.integers(1, 4))
+        prec = "f64" if rng.random() < 0.5 else "f32"
+        n = int(rng.choice([1, 7, 255, 257, 4097, 75_777, 300_001]))
+        cp, cv = GASES[int(rng.integers(0, len(GASES)))]
+        gas, og = fvb.Gas(cp[0], cp[1], cv[0], cv[1]), orc.gas(cp=cp, cv=cv)
+        pinned = bool(rng.random() < 0.5)
+        ctx = fvb.HostContext(0, chunk_points=int(rng.choice([256, 1024, 65_536, 0])))
+        s_np = orc.random_state(dim, n, seed=int(rng.integers(1, 1 << 30)), prec=prec)
+        hs = [torch.from_numpy(a) for a in s_np]
+        count = (dim + 2) * dim if block == "flux" else dim * (dim + 2) ** 2
+        outs = [torch.full((n,), float("nan"), dtype=DT[prec]) for _ in range(count)]
+        if pinned:
+            hs = [t.pin_memory() for t in hs]
+            outs = [t.pin_memory() for t in outs]
+        what = (block, dim, prec, n, cp, cv, pinned)
+        if block == "flux":
+            ctx.flux(hs, dim, outs, gas=gas)
+            want = orc.flux(dim, s_np, gas=og)
+        else:
+            _, lam = ctx.jacobian(hs, dim, outs, gas=gas)
+            want, lam_w = orc.jacobian(dim, s_np, gas=og)
+            assert lam == lam_w, what
+        assert all(o.numpy().tobytes() == np.asarray(w).tobytes() for o, w in zip(outs, want)), what
+        ctx.close()
