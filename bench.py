@@ -74,6 +74,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=10_000_000,
                     help="points per reference step (bounded CPU sample)")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="CPU work the cpu_baseline leg aims for (reps of the sample)")
     ap.add_argument("--out", default="", help="also append the JSON line to this file")
     a = ap.parse_args()
     if a.warmup < 3:
@@ -454,12 +456,16 @@ def device_run(a, rank, world, local):
             sample = min(n, a.cpu_sample if a.config != "axpy" else n)
             if a.config == "jacobian3d":
                 sample = min(sample, 2_000_000)
-            pts, times = reference_run(a.config, a.prec, 3, 1, sample, threads)
+            # a probe rep sizes the run to about a.cpu_seconds of CPU work
+            _, probe = reference_run(a.config, a.prec, 1, 1, sample, threads)
+            reps = int(min(500, max(3, a.cpu_seconds / max(probe[0] * 1e-9, 1e-6))))
+            pts, times = reference_run(a.config, a.prec, reps, 1, sample, threads)
             med = statistics.median(times)
             cpu = {"value": pts / (med * 1e-9) / 1e9, "unit": "Gpoints/s", "cores": threads,
                    "kind": "reference",
-                   "sample": f"{pts} points of the same workload per rep, median of 3 reps "
-                             f"after 1 JIT warm-up, Backend::parallel(0, {threads})"}
+                   "sample": f"{pts} points of the same workload per rep, median of {reps} reps "
+                             f"({sum(times) * 1e-9:.1f} s of CPU work) after 1 JIT warm-up, "
+                             f"Backend::parallel(0, {threads})"}
         except Exception as ex:  # reported, never a substitute for the device number
             cpu = {"value": None, "unit": "Gpoints/s", "cores": cpu_threads(),
                    "kind": "reference", "sample": f"unavailable: {ex}"}
