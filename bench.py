@@ -261,15 +261,18 @@ def end_to_end(a, fvb, ins, n, n_in, n_out, dim, dt, esize, local, dist, world, 
         e2e_s = te.item()
     ctx.close()
     # planes written host-side instead of crossing PCIe: the flux's row 0
-    # (copies of the momentum inputs) and the Jacobian's constant entries
+    # (copies of the momentum inputs), the Jacobian's constant entries
     # (JacobianOp::constant_item: 4 / 12 / 30 of 9 / 32 / 75 in 1-/2-/3-D)
+    # and its duplicate entries (JacobianOp::duplicate_of: 0 / 4 / 18), copied
+    # host-side from the shipped copy
     passthrough = dim if a.config == "flux3d" else 0
     filled = {1: 4, 2: 12, 3: 30}[dim] if a.config == "jacobian3d" else 0
+    dups = {1: 0, 2: 4, 3: 18}[dim] if a.config == "jacobian3d" else 0
     return {"value": world * n / e2e_s / 1e9, "unit": "Gpoints/s",
             "h2d_bytes_per_step": world * n * n_in * esize,
-            "d2h_bytes_per_step": world * n * (n_out - passthrough - filled) * esize
+            "d2h_bytes_per_step": world * n * (n_out - passthrough - filled - dups) * esize
                                   + (8 if a.config == "jacobian3d" else 0),
-            "host_passthrough_bytes_per_step": world * n * passthrough * esize,
+            "host_passthrough_bytes_per_step": world * n * (passthrough + dups) * esize,
             "host_fill_bytes_per_step": world * n * filled * esize,
             "ms_per_step": e2e_s * 1e3, "host_memory": "pinned", "steps": a.e2e_steps,
             "points_per_rank": n,

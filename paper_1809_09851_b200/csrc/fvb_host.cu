@@ -222,6 +222,8 @@ struct Arg {
     bool out = false;
     int alias = -1;        // output: index of the host input whose staging it shares
     bool scratch = false;  // output with a device slot only (written, never copied back)
+    char* dup_dst = nullptr;  // scratch output copied host-side from output args[dup_of]
+    int dup_of = -1;
     // assigned by staged():
     bool pinned = false;
     size_t dev_off = 0, pin_off = 0;  // byte offsets of the plane in a slot, per chunk element
@@ -292,7 +294,9 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
         for (Arg& a : args) a.has_pin = false;
         any_pageable = false;
     }
-    if (any_pageable && !ctx->pool) {
+    bool any_dup = false;
+    for (const Arg& a : args) any_dup |= a.dup_of >= 0;
+    if ((any_pageable || any_dup) && !ctx->pool) {
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         ctx->pool.reset(new (std::nothrow) CopyPool(std::min(16u, hw) - 1));
     }
@@ -329,6 +333,14 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
             if (a.out && a.host && a.has_pin)
                 add_pieces(pieces, a.host + off * a.width, pin + a.pin_off * chunk, cnt * a.width);
         copy(pieces);
+        if (any_dup) {  // duplicate outputs: from their (now complete) source output
+            pieces.clear();
+            for (const Arg& a : args)
+                if (a.dup_of >= 0)
+                    add_pieces(pieces, a.dup_dst + off * a.width,
+                               args[size_t(a.dup_of)].host + off * a.width, cnt * a.width);
+            copy(pieces);
+        }
         return FVB_OK;
     };
 
@@ -379,7 +391,7 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
                 cudaMemcpyAsync(dst, dargs[i], cnt * a.width, cudaMemcpyDeviceToHost, s);
             if (e != cudaSuccess) return cuda_fail(e, "device->host copy");
         }
-        if (unpack) {
+        if (unpack || any_dup) {
             const cudaError_t e = cudaEventRecord(ctx->done[slot], s);
             if (e != cudaSuccess) return cuda_fail(e, "chunk event");
             pending[slot] = int64_t(c);
@@ -401,6 +413,9 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
 //    include/fusevec/fluid.hpp:168-169); the host already holds those bytes;
 //  - constant items (the Jacobian's 0 / 1 / gamma-1 entries, 30 of 75 in
 //    3-D): every element is the same value of T, filled in place.
+// (Duplicate items -- JacobianOp::duplicate_of, 18 of 75 -- are copied
+// host-side too, but per chunk, once their source output has landed: the
+// staged executor's dup_of.)
 // Joined on every exit path.
 struct HostJob {
     char* dst;
@@ -505,6 +520,7 @@ fvb_status pipeline(fvb_ctx* ctx, const void* const* in, void* const* out, uint6
             host_side.push_back({static_cast<char*>(out[j]),
                                  static_cast<const char*>(in[1 + j]), 0});
         }
+        int dup = -1;
         if constexpr (FILL) {
             T v;
             if (!on_host && Op::constant_item(j, k, &v)) {
@@ -512,10 +528,16 @@ fvb_status pipeline(fvb_ctx* ctx, const void* const* in, void* const* out, uint6
                 std::memcpy(&bits, &v, sizeof v);
                 host_side.push_back({static_cast<char*>(out[j]), nullptr, bits});
                 on_host = true;
+            } else if (!on_host) {
+                dup = Op::duplicate_of(j);  // an earlier, computed and shipped output
             }
         }
-        Arg a{on_host ? nullptr : static_cast<char*>(out[j]), nullptr, sizeof(T), true};
-        a.scratch = on_host;
+        Arg a{on_host || dup >= 0 ? nullptr : static_cast<char*>(out[j]), nullptr, sizeof(T), true};
+        a.scratch = on_host || dup >= 0;
+        if (dup >= 0) {
+            a.dup_dst = static_cast<char*>(out[j]);
+            a.dup_of = NIN + dup;
+        }
         args.push_back(a);
     }
     HostSide<T> host_writes(host_side, size_t(n) * sizeof(T));

@@ -300,6 +300,42 @@ struct JacobianOp {
         }
         return false;
     }
+    // Items computed by the same expression as an earlier item (18 of the 45
+    // non-constant ones in 3-D): u_m appears four times (t0- or t1-only
+    // momentum entries), -(gm1*u_m) twice, and -(u_i*u_k) and
+    // -(gm1*(u_j*u_k)) once per direction of the pair (IEEE products are
+    // commutative, so both orders give the same bits).  The host-buffer
+    // path ships one copy over PCIe and copies it host-side.
+    __host__ __device__ static int value_id(int item) {
+        const int dir = item / (W * W);
+        const int r = (item / W) % W;
+        const int c = item % W;
+        if (r >= 1 && r <= D) {
+            const int i = r - 1;
+            if (c >= 1 && c <= D) {
+                const int j = c - 1;
+                const bool t0 = (i == j), t1 = (j == dir), t2 = (i == dir);
+                if (t0 && !t1 && !t2) return 16 + dir;  // u_dir
+                if (t1 && !t0 && !t2) return 16 + i;    // u_i
+                if (t2 && !t0 && !t1) return 32 + j;    // -(gm1*u_j)
+                return -1;
+            }
+            if (c == 0 && i != dir) return 48 + 4 * (i < dir ? i : dir) + (i < dir ? dir : i);
+            return -1;
+        }
+        if (r == W - 1 && c >= 1 && c <= D && c - 1 != dir) {
+            const int j = c - 1;
+            return 64 + 4 * (j < dir ? j : dir) + (j < dir ? dir : j);
+        }
+        return -1;
+    }
+    __host__ __device__ static int duplicate_of(int item) {
+        const int id = value_id(item);
+        if (id < 0) return -1;
+        for (int e = 0; e < item; ++e)
+            if (value_id(e) == id) return e;
+        return -1;
+    }
     __device__ __forceinline__ static T out(const State& s, int item, const Consts<T>& k) {
         T cv;
         if (constant_item(item, k, &cv)) return cv;
