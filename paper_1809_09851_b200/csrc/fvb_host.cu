@@ -573,6 +573,55 @@ fvb_status pipeline_dim(fvb_ctx* ctx, const fvb_gas* gas, uint32_t dim, const vo
     }
 }
 
+// fvb_launch_host with a hand-written Jacobian kernel (the reference's
+// Jacobian block through the adapter or the JIT seam): the same host-side
+// treatment as fvb_jacobian_host -- constant entries filled by host threads,
+// duplicate entries shipped once and copied per chunk -- for host output
+// slots that alias no input.  Both are exactly what the kernel would write
+// (its own Consts, JacobianOp's own item tables).
+template <class T, int D>
+void jacobian_host_side(const fvb_kernel* k, std::vector<Arg>& v, std::vector<HostJob>& fills) {
+    using Op = JacobianOp<T, D>;
+    if (k->n_outputs != uint32_t(Op::NOUT)) return;
+    const Consts<T> c{static_cast<T>(k->consts[0]), static_cast<T>(k->consts[1]),
+                      static_cast<T>(k->consts[2]), static_cast<T>(k->consts[3]),
+                      static_cast<T>(k->consts[4]), static_cast<T>(k->consts[5])};
+    for (int j = 0; j < Op::NOUT; ++j) {
+        Arg& a = v[size_t(j)];
+        if (!a.host || a.alias >= 0 || a.width != sizeof(T)) continue;
+        T val;
+        if (Op::constant_item(j, c, &val)) {
+            uint64_t bits = 0;
+            std::memcpy(&bits, &val, sizeof val);
+            fills.push_back({a.host, nullptr, bits});
+            a.host = nullptr;
+            a.scratch = true;
+            continue;
+        }
+        const int d = Op::duplicate_of(j);
+        if (d < 0) continue;
+        const Arg& src = v[size_t(d)];
+        if (!src.host || src.alias >= 0 || src.dup_of >= 0 || src.width != sizeof(T)) continue;
+        a.dup_dst = a.host;
+        a.dup_of = d;
+        a.host = nullptr;
+        a.scratch = true;
+    }
+}
+
+void launch_host_side(const fvb_kernel* k, std::vector<Arg>& v, std::vector<HostJob>& fills) {
+    if (k->impl || std::strncmp(k->name, "jacobian", 8) != 0) return;
+    switch (k->dim * 2 + k->prec) {
+        case 2: return jacobian_host_side<float, 1>(k, v, fills);
+        case 3: return jacobian_host_side<double, 1>(k, v, fills);
+        case 4: return jacobian_host_side<float, 2>(k, v, fills);
+        case 5: return jacobian_host_side<double, 2>(k, v, fills);
+        case 6: return jacobian_host_side<float, 3>(k, v, fills);
+        case 7: return jacobian_host_side<double, 3>(k, v, fills);
+        default: return;
+    }
+}
+
 fvb_status check(fvb_ctx* ctx, const fvb_gas* gas, uint32_t dim, uint8_t prec) {
     if (!ctx) return fail(FVB_EARG, "NULL context");
     if (prec > 1) return fail(FVB_EPREC, "precision code must be 0 (f32) or 1 (f64)");
@@ -724,10 +773,19 @@ fvb_status fvb_launch_host(fvb_ctx* ctx, const fvb_kernel* k, uint64_t n, void* 
             if (lambda_max) *lambda_max = 0.0;
             return FVB_OK;
         }
-        fvb_status st = staged(ctx, v, n, [&](void* const* d, uint64_t cnt, cudaStream_t s) {
-            if (lambda_max) return k->reduce(k, 0, cnt, d, ctx->red, s);
-            return k->fn(k, 0, cnt, d, s);
-        });
+        std::vector<HostJob> fills;
+        launch_host_side(k, v, fills);
+        fvb_status st;
+        {
+            // fills run on host threads while the pipeline streams; joined
+            // (on every exit) before the call returns
+            HostSide<double> fill_d(k->prec ? fills : std::vector<HostJob>{}, n * 8);
+            HostSide<float> fill_f(k->prec ? std::vector<HostJob>{} : fills, n * 4);
+            st = staged(ctx, v, n, [&](void* const* d, uint64_t cnt, cudaStream_t s) {
+                if (lambda_max) return k->reduce(k, 0, cnt, d, ctx->red, s);
+                return k->fn(k, 0, cnt, d, s);
+            });
+        }
         if (st) return st;
         if (lambda_max) return red_bytes == 8 ? read_lambda<double>(ctx, lambda_max)
                                               : read_lambda<float>(ctx, lambda_max);

@@ -1144,6 +1144,23 @@ void run_perf(std::size_t n) {
     const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / reps;
     std::printf("{\"path\": \"evaluate_block, resident leaves, tie'd device outputs\", \"points\": %zu, "
                 "\"ms\": %.3f, \"gpts\": %.4f}\n", n, s * 1e3, n / s / 1e9);
+    // the Jacobian block + CFL from and into host DenseVectors (pageable):
+    // 30 constant entries filled and 18 duplicates copied host-side
+    {
+        const std::size_t nj = std::min<std::size_t>(n, 5'000'000);
+        SplitMix64 rj(0x5EED);
+        auto fj = random_state(3, nj, rj);
+        StateSet uj = state_conservative(EosSpec(), 3, leaves_of(fj));
+        BlockVectorGrid jg(15, 5, Precision::f64, nj);
+        (void)dev::evaluate_block_cfl(be, inviscid_flux_jacobian(uj), jg);  // warm
+        const int rj_reps = 3;
+        auto tj0 = std::chrono::steady_clock::now();
+        for (int r = 0; r < rj_reps; ++r) (void)dev::evaluate_block_cfl(be, inviscid_flux_jacobian(uj), jg);
+        const double sj =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - tj0).count() / rj_reps;
+        std::printf("{\"path\": \"evaluate_block_cfl(jacobian), host DenseVectors (pageable) in and out\", "
+                    "\"points\": %zu, \"ms\": %.3f, \"gpts\": %.4f}\n", nj, sj * 1e3, nj / sj / 1e9);
+    }
 }
 
 // Host overhead of one reference-API call at small n: the adapter's key

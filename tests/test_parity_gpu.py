@@ -432,6 +432,43 @@ def test_launch_host_any_kernel(cuda, orc, mode):
     ctx.close()
 
 
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("pinned", [False, True])
+def test_launch_host_jacobian_host_side_writes(cuda, orc, prec, pinned):
+    # fvb_launch_host with the hand-written Jacobian kernel (the reference's
+    # Jacobian block through the adapter or the JIT seam): its constant
+    # entries are filled and its duplicate entries copied host-side.  Outputs
+    # start as NaN, so a skipped host-side write shows; a non-default gas
+    # (another gamma-1), d = 2 and 3, a CFL reduction, several chunks; one
+    # output on the device and one output slot aliasing nothing special.
+    import re
+    import struct
+    g, og = fvb.Gas(5, 2, 3, 2), orc.gas(cp=(5, 2), cv=(3, 2))
+    consts = {"half": 0.5, "gm1": g.gamma_minus_one, "gamma": g.gamma, "zero": 0.0, "one": 1.0}
+    c = "d" if prec == "f64" else "s"
+    ctx = fvb.HostContext(0, chunk_points=1 << 14)
+    for dim in (2, 3):
+        n = 100_003
+        k = fvb.lookup(re.sub(r"C([sd])#(\w+);", lambda m: "C%s%016x;" % (m.group(1), struct.unpack(
+            "<Q", struct.pack("<d", consts[m.group(2)]))[0]),
+            dict(fvb.patterns())[f"jacobian{dim}_{prec}"]))
+        assert k.name.decode().startswith("jacobian")
+        s_np = orc.random_state(dim, n, seed=40 + dim, prec=prec)
+        want, lam_w = orc.jacobian(dim, s_np, gas=og)
+        leaves = [None] * k.n_inputs
+        for ci in range(k.n_inputs):
+            leaves[k.in_slot[ci]] = torch.from_numpy(s_np[ci])
+        outs = [torch.full((n,), float("nan"), dtype=DT[prec]) for _ in range(k.n_outputs)]
+        if pinned:
+            leaves = [t.pin_memory() for t in leaves]
+            outs = [t.pin_memory() for t in outs]
+        outs[1] = outs[1].to(cuda)  # row 0, column 1 (a constant entry) on the device
+        lam = ctx.launch(k, outs + leaves, n, reduce=True)
+        assert lam == lam_w, dim
+        assert all_same([t.cpu().numpy() for t in outs], want), (dim, c)
+    ctx.close()
+
+
 # ---- structural-key kernels -----------------------------------------------------------
 
 
