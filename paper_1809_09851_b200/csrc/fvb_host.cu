@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "fvb.h"
+#include "fvb_hostcopy.h"
 #include "fvb_launch.cuh"
 
 namespace fvb {
@@ -58,7 +59,7 @@ class CopyPool {
     void run(const std::vector<Piece>& pieces) {
         if (pieces.empty()) return;
         if (threads_.empty() || pieces.size() == 1) {
-            for (const Piece& p : pieces) std::memcpy(p.dst, p.src, p.bytes);
+            for (const Piece& p : pieces) host_copy(p.dst, p.src, p.bytes);
             return;
         }
         {
@@ -78,7 +79,7 @@ class CopyPool {
   private:
     void drain(const std::vector<Piece>& pieces) {
         for (size_t i; (i = next_.fetch_add(1)) < pieces.size();)
-            std::memcpy(pieces[i].dst, pieces[i].src, pieces[i].bytes);
+            host_copy(pieces[i].dst, pieces[i].src, pieces[i].bytes);
     }
     void loop() {
         uint64_t seen = 0;
@@ -304,7 +305,7 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
         if (ctx->pool)
             ctx->pool->run(p);
         else
-            for (const Piece& q : p) std::memcpy(q.dst, q.src, q.bytes);
+            for (const Piece& q : p) host_copy(q.dst, q.src, q.bytes);
     };
 
     // On every exit -- an error part-way included -- nothing this call
@@ -437,15 +438,10 @@ struct HostSide {
                 const HostJob& j = jobs[lo / bytes];
                 const size_t at = lo % bytes;
                 const size_t len = std::min(hi - lo, bytes - at);
-                if (j.src) {
-                    std::memcpy(j.dst + at, j.src + at, len);
-                } else if (j.fill == 0) {
-                    std::memset(j.dst + at, 0, len);
-                } else {
-                    T v;
-                    std::memcpy(&v, &j.fill, sizeof v);
-                    std::fill_n(reinterpret_cast<T*>(j.dst + at), len / sizeof(T), v);
-                }
+                if (j.src)
+                    host_copy(j.dst + at, j.src + at, len);
+                else
+                    host_fill(j.dst + at, j.fill, sizeof(T), len);
                 lo += len;
             }
         };
