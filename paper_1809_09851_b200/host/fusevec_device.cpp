@@ -846,10 +846,14 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
             for (const Out& w : plan.outs) uses += w.host == d;
             return uses == 1;
         };
+        // (The hand-written Jacobian's constant and duplicate entries are
+        // written host-side by fvb_launch_host itself, with streaming stores.)
+        const bool lib_fills = !plan.k.impl && std::strncmp(plan.k.name, "jacobian", 8) == 0;
         for (std::size_t j = 0; j < items.size(); ++j) {
             const Out& o = plan.outs[j];
             if (!o.host || !exclusive(o.host)) continue;
-            if (bare_constant(items[j].node(), o.host->precision(), &plan.fill_bits[j])) {
+            if (!lib_fills &&
+                bare_constant(items[j].node(), o.host->precision(), &plan.fill_bits[j])) {
                 plan.has_fill[j] = 1;
                 continue;
             }
