@@ -496,6 +496,13 @@ fvb_status pipeline(fvb_ctx* ctx, const void* const* in, void* const* out, uint6
     if (plane_overlap(in, NIN, const_cast<const void* const*>(out), NOUT, size_t(n) * sizeof(T)) !=
         kDisjoint)
         return fail(FVB_EARG, "host output plane overlaps an input plane");
+    if (PASS > 0 || FILL) {  // host threads write some outputs while the pipeline writes others
+        std::vector<uintptr_t> starts;
+        for (int j = 0; j < NOUT; ++j) starts.push_back(reinterpret_cast<uintptr_t>(out[j]));
+        std::sort(starts.begin(), starts.end());
+        if (std::adjacent_find(starts.begin(), starts.end()) != starts.end())
+            return fail(FVB_EARG, "two host outputs name one plane");
+    }
     DeviceGuard guard(ctx->device);
     using Bu = typename Bits<T>::U;
     if (RED)

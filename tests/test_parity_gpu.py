@@ -341,6 +341,23 @@ def test_host_path_matches_device(cuda, orc, pinned):
     ctx.close()
 
 
+def test_host_path_rejects_one_plane_for_two_outputs(cuda, orc):
+    # host threads write the pass-through / constant outputs while the
+    # pipeline writes the rest: one plane named twice would race
+    s_np = orc.random_state(3, 1000, seed=3)
+    hs = [torch.from_numpy(a) for a in s_np]
+    ctx = fvb.HostContext(0)
+    outs = [torch.empty(1000, dtype=torch.float64) for _ in range(75)]
+    outs[40] = outs[7]
+    with pytest.raises(fvb.ArgumentError):
+        ctx.jacobian(hs, 3, outs)
+    fo = [torch.empty(1000, dtype=torch.float64) for _ in range(15)]
+    fo[0] = fo[9]
+    with pytest.raises(fvb.ArgumentError):
+        ctx.flux(hs, 3, fo)
+    ctx.close()
+
+
 @pytest.mark.parametrize("prec", ["f64", "f32"])
 def test_host_jacobian_constant_fills(cuda, orc, prec):
     # the constant entries (0, 1, gamma-1) are filled by host threads: every
