@@ -26,6 +26,15 @@ fvb_status cuda_fail(cudaError_t e, const char* what);
 
 int device_sm_count();
 
+// Programmatic dependent launch of the pointwise kernels (FVB_PDL=0: off).
+inline bool pdl_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("FVB_PDL");
+        return !(e && e[0] == '0' && e[1] == '\0');
+    }();
+    return v;
+}
+
 // No C++ exception crosses the C ABI: entry points whose host side
 // allocates (keys, NVRTC, host threads) run their body under this guard.
 template <class F>
@@ -174,8 +183,22 @@ fvb_status launch_fixed(const Planes<T, Op::NIN, Op::NOUT>& pl, const Consts<T>&
     }
     if (grid == 0) grid = 1;  // block 0 still handles the scalar head/tail
     if (grid > 0x7fffffffull) return fail(FVB_EARG, "range too large for one launch");
-    kern<<<unsigned(grid), unsigned(THREADS), 0, stream>>>(pl, k, rg, red);
-    const cudaError_t e = cudaGetLastError();
+    // Programmatic dependent launch: back-to-back evaluations (a time step's
+    // blocks, a CUDA graph of them) overlap one grid's launch with the
+    // previous grid's tail; the kernel's griddepcontrol.wait keeps the
+    // stream order of every byte.  FVB_PDL=0 launches plainly.
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(unsigned(THREADS));
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, pl, k, rg, red);
+    const cudaError_t e = le != cudaSuccess ? le : cudaGetLastError();
     return e == cudaSuccess ? FVB_OK : cuda_fail(e, "kernel launch");
 }
 

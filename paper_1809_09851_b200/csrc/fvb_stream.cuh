@@ -338,6 +338,11 @@ __global__ void __launch_bounds__(THREADS, MINB)
     pointwise_kernel(const Planes<T, Op::NIN, Op::NOUT> pl, const Consts<T> k, const Range rg,
                      typename Bits<T>::U* __restrict__ red) {
     using Bu = typename Bits<T>::U;
+    // Programmatic dependent launch (launch_fixed): this grid may have been
+    // scheduled while the previous one on the stream was still draining.
+    // Wait for it to complete (its memory visible) before touching any
+    // plane; a no-op for an ordinary launch.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     Bu acc = 0;
     if (MODE == kTiles) {
         const uint64_t g0 = uint64_t(blockIdx.x) * (uint64_t(THREADS) * U) + threadIdx.x;
@@ -372,6 +377,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
             }
         }
     }
+    // This CTA's work is issued: the next grid may begin launching (it
+    // still waits for this whole grid in its griddepcontrol.wait).
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 }  // namespace fvb
