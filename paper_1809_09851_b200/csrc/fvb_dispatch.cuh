@@ -22,16 +22,19 @@ inline fvb_status check_gas(const fvb_gas* g) {
     return FVB_OK;
 }
 
+// reset_red: the reduction word is zeroed (after validation) before the
+// kernel accumulates into it.
 template <template <class, int> class OpT, bool RED, bool TUNE3, class T>
 fvb_status run_dim(uint32_t dim, const void* const* in, void* const* out, uint64_t n,
-                   const fvb_gas* gas, typename Bits<T>::U* red, cudaStream_t s) {
+                   const fvb_gas* gas, typename Bits<T>::U* red, cudaStream_t s,
+                   bool reset_red = false) {
     const auto k = make_consts<T>(gas);
     auto i = reinterpret_cast<const T* const*>(in);
     auto o = reinterpret_cast<T* const*>(out);
     switch (dim) {
-        case 1: return launch_op<OpT<T, 1>, T, RED, false>(i, o, n, k, red, s);
-        case 2: return launch_op<OpT<T, 2>, T, RED, false>(i, o, n, k, red, s);
-        default: return launch_op<OpT<T, 3>, T, RED, TUNE3>(i, o, n, k, red, s);
+        case 1: return launch_op<OpT<T, 1>, T, RED, false>(i, o, n, k, red, s, reset_red);
+        case 2: return launch_op<OpT<T, 2>, T, RED, false>(i, o, n, k, red, s, reset_red);
+        default: return launch_op<OpT<T, 3>, T, RED, TUNE3>(i, o, n, k, red, s, reset_red);
     }
 }
 
@@ -39,14 +42,6 @@ template <class T, int D>
 using WaveSpeed0 = WaveSpeedOp<T, D, 0>;
 template <class T, int D>
 using WaveSpeed1 = WaveSpeedOp<T, D, 1>;
-
-// Reset the device scalar, then let the kernel atomic-max into it (all in
-// stream order, so concurrent calls on different outputs never interfere).
-template <class T>
-fvb_status reset_scalar(void* p, cudaStream_t s) {
-    const cudaError_t e = cudaMemsetAsync(p, 0, sizeof(T), s);
-    return e == cudaSuccess ? FVB_OK : cuda_fail(e, "lambda_max reset");
-}
 
 unsigned simple_grid(uint64_t n);
 

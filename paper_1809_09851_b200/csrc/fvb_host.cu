@@ -359,6 +359,10 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
         for (const Arg& a : args)
             if (!a.out && a.host && a.has_pin)
                 add_pieces(pieces, pin + a.pin_off * chunk, a.host + off * a.width, cnt * a.width);
+        // the slot's bounce buffer is then busy until this chunk's copies
+        // complete: the next chunk on this slot must wait for them even when
+        // no output is unpacked from it
+        const bool packed = !pieces.empty();
         copy(pieces);
         for (size_t i = 0; i < args.size(); ++i) {
             const Arg& a = args[i];
@@ -392,7 +396,7 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
                 cudaMemcpyAsync(dst, dargs[i], cnt * a.width, cudaMemcpyDeviceToHost, s);
             if (e != cudaSuccess) return cuda_fail(e, "device->host copy");
         }
-        if (unpack || any_dup) {
+        if (unpack || any_dup || packed) {
             const cudaError_t e = cudaEventRecord(ctx->done[slot], s);
             if (e != cudaSuccess) return cuda_fail(e, "chunk event");
             pending[slot] = int64_t(c);

@@ -16,6 +16,8 @@ using namespace fvb;
 
 extern "C" {
 
+// The CFL word is zeroed in stream order (so concurrent calls on different
+// words never interfere) by launch_op, once the planes have been validated.
 fvb_status fvb_jacobian(const fvb_gas* gas, uint32_t dim, uint8_t prec, uint64_t n,
                         const void* const* in, void* const* out, void* lambda_max,
                         void* stream) {
@@ -26,15 +28,13 @@ fvb_status fvb_jacobian(const fvb_gas* gas, uint32_t dim, uint8_t prec, uint64_t
     if (prec == FVB_F64) {
         if (!lambda_max)
             return run_dim<JacobianOp, false, false, double>(dim, in, out, n, gas, nullptr, s);
-        if (fvb_status st = reset_scalar<double>(lambda_max, s)) return st;
         return run_dim<JacobianOp, true, false, double>(
-            dim, in, out, n, gas, static_cast<unsigned long long*>(lambda_max), s);
+            dim, in, out, n, gas, static_cast<unsigned long long*>(lambda_max), s, true);
     }
     if (!lambda_max)
         return run_dim<JacobianOp, false, false, float>(dim, in, out, n, gas, nullptr, s);
-    if (fvb_status st = reset_scalar<float>(lambda_max, s)) return st;
     return run_dim<JacobianOp, true, false, float>(dim, in, out, n, gas,
-                                                  static_cast<unsigned int*>(lambda_max), s);
+                                                  static_cast<unsigned int*>(lambda_max), s, true);
 }
 
 fvb_status fvb_wave_speed_max(const fvb_gas* gas, uint32_t dim, uint8_t prec, uint64_t n,
@@ -47,15 +47,14 @@ fvb_status fvb_wave_speed_max(const fvb_gas* gas, uint32_t dim, uint8_t prec, ui
     auto s = static_cast<cudaStream_t>(stream);
     void* const outs[1] = {lambda};
     if (prec == FVB_F64) {
-        if (fvb_status st = reset_scalar<double>(lambda_max, s)) return st;
         auto red = static_cast<unsigned long long*>(lambda_max);
-        if (lambda) return run_dim<WaveSpeed1, true, false, double>(dim, in, outs, n, gas, red, s);
-        return run_dim<WaveSpeed0, true, true, double>(dim, in, outs, n, gas, red, s);
+        if (lambda)
+            return run_dim<WaveSpeed1, true, false, double>(dim, in, outs, n, gas, red, s, true);
+        return run_dim<WaveSpeed0, true, true, double>(dim, in, outs, n, gas, red, s, true);
     }
-    if (fvb_status st = reset_scalar<float>(lambda_max, s)) return st;
     auto red = static_cast<unsigned int*>(lambda_max);
-    if (lambda) return run_dim<WaveSpeed1, true, false, float>(dim, in, outs, n, gas, red, s);
-    return run_dim<WaveSpeed0, true, true, float>(dim, in, outs, n, gas, red, s);
+    if (lambda) return run_dim<WaveSpeed1, true, false, float>(dim, in, outs, n, gas, red, s, true);
+    return run_dim<WaveSpeed0, true, true, float>(dim, in, outs, n, gas, red, s, true);
 }
 
 }  // extern "C"

@@ -209,12 +209,22 @@ constexpr int vec32() {
 
 // Dispatch on the tuning knobs.  Only the headline kernels (TUNABLE) get the
 // full variant set; everything else runs the default configuration.
+// reset_red: zero the reduction word in stream order first (a fresh CFL
+// maximum; the staged host path accumulates over chunks and resets it once
+// itself) -- only after every plane has been validated, so a refused call
+// enqueues nothing and leaves the caller's word alone.
 template <class Op, class T, bool RED, bool TUNABLE>
 fvb_status launch_op(const T* const* in, T* const* out, uint64_t n, const Consts<T>& k,
-                     typename Bits<T>::U* red, cudaStream_t stream) {
+                     typename Bits<T>::U* red, cudaStream_t stream, bool reset_red = false) {
+    auto reset = [&]() -> fvb_status {
+        if (!RED || !reset_red) return FVB_OK;
+        const cudaError_t e = cudaMemsetAsync(red, 0, sizeof(*red), stream);
+        return e == cudaSuccess ? FVB_OK : cuda_fail(e, "lambda_max reset");
+    };
     // n == 0 is a no-op even with NULL planes (an empty torch tensor or
-    // DenseVector has no storage), as evaluate() returns early for n == 0.
-    if (n == 0) return FVB_OK;
+    // DenseVector has no storage), as evaluate() returns early for n == 0;
+    // a reduction over nothing is 0.
+    if (n == 0) return reset();
     Planes<T, Op::NIN, Op::NOUT> pl;
     const void* ptrs[Op::NIN + (Op::NOUT > 0 ? Op::NOUT : 1)];
     int np = 0;
@@ -245,6 +255,7 @@ fvb_status launch_op(const T* const* in, T* const* out, uint64_t n, const Consts
         default:
             break;
     }
+    if (fvb_status st = reset()) return st;
 
     constexpr int VD = vec32<T>();
     const Tuning& t = tuning();

@@ -66,18 +66,41 @@ def _gas_ptr(gas: Optional[Gas]):
     return ctypes.byref(gas.struct())
 
 
-def _stream(stream) -> int:
+def _stream(stream, device=None) -> int:
+    """The CUDA stream handle to enqueue on: `stream`, else the current torch
+    stream of `device` (the planes' device), not of the current device."""
     if stream is None:
-        return torch.cuda.current_stream().cuda_stream
+        return torch.cuda.current_stream(device).cuda_stream
     return getattr(stream, "cuda_stream", stream)
 
 
+def _scalar_out(t, prec: int, device, what: str) -> int:
+    """Pointer of a caller-supplied lambda_max accumulator.  The kernel
+    memsets and atomicMax-es one element of the state's precision there, so
+    anything else (a CPU tensor, another GPU, a narrower dtype, no element)
+    would be an out-of-bounds or foreign device write: refused up front."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise N.ArgumentError(N.FVB_EARG, f"{what}: must be a CUDA tensor")
+    if t.device != torch.device(device):
+        raise N.ArgumentError(N.FVB_EARG, f"{what}: on {t.device}, the state is on {device}")
+    if t.dtype != _DTYPE[prec]:
+        raise N.PrecisionError(N.FVB_EPREC, f"{what}: dtype {t.dtype}, the state is "
+                                            f"{_DTYPE[prec]}")
+    if t.numel() < 1:
+        raise N.ArgumentError(N.FVB_EARG, f"{what}: needs one element")
+    return t.data_ptr()
+
+
 def _planes(planes: Sequence[torch.Tensor], what: str, n: Optional[int] = None,
-            prec: Optional[int] = None):
+            prec: Optional[int] = None, device=None):
     ptrs = []
+    device = planes[0].device if device is None and len(planes) else device
     for t in planes:
         if not isinstance(t, torch.Tensor) or not t.is_cuda:
             raise N.ArgumentError(N.FVB_EARG, f"{what}: planes must be CUDA tensors")
+        if t.device != device:
+            raise N.ArgumentError(N.FVB_EARG, f"{what}: a plane on {t.device}, expected "
+                                              f"{device}")
         if t.dim() != 1 or not t.is_contiguous():
             raise N.ArgumentError(N.FVB_EARG, f"{what}: planes must be contiguous 1-D")
         p = _PREC.get(t.dtype)
@@ -113,9 +136,10 @@ def flux(state: Sequence[torch.Tensor], dim: int, out=None, gas: Optional[Gas] =
     ins, n, prec = _state(state, dim)
     if out is None:
         out = _alloc((dim + 2) * dim, n, prec, state[0].device)
-    outs, _, _ = _planes(out, "flux out", n, prec)
-    N.check(N.lib().fvb_flux(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins), N.ptr_array(outs),
-                             _stream(stream)))
+    outs, _, _ = _planes(out, "flux out", n, prec, device=state[0].device)
+    with torch.cuda.device(state[0].device):
+        N.check(N.lib().fvb_flux(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins), N.ptr_array(outs),
+                                 _stream(stream, state[0].device)))
     return out
 
 
@@ -124,9 +148,10 @@ def flux_prim(prim, dim, out=None, gas=None, stream=None):
     ins, n, prec = _state(prim, dim)
     if out is None:
         out = _alloc((dim + 2) * dim, n, prec, prim[0].device)
-    outs, _, _ = _planes(out, "flux_prim out", n, prec)
-    N.check(N.lib().fvb_flux_prim(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins),
-                                  N.ptr_array(outs), _stream(stream)))
+    outs, _, _ = _planes(out, "flux_prim out", n, prec, device=prim[0].device)
+    with torch.cuda.device(prim[0].device):
+        N.check(N.lib().fvb_flux_prim(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins),
+                                      N.ptr_array(outs), _stream(stream, prim[0].device)))
     return out
 
 
@@ -135,9 +160,10 @@ def cons2prim(state, dim, out=None, gas=None, stream=None):
     ins, n, prec = _state(state, dim)
     if out is None:
         out = _alloc(dim + 2, n, prec, state[0].device)
-    outs, _, _ = _planes(out, "cons2prim out", n, prec)
-    N.check(N.lib().fvb_cons2prim(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins),
-                                  N.ptr_array(outs), _stream(stream)))
+    outs, _, _ = _planes(out, "cons2prim out", n, prec, device=state[0].device)
+    with torch.cuda.device(state[0].device):
+        N.check(N.lib().fvb_cons2prim(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins),
+                                      N.ptr_array(outs), _stream(stream, state[0].device)))
     return out
 
 
@@ -146,9 +172,10 @@ def prim2cons(prim, dim, out=None, gas=None, stream=None):
     ins, n, prec = _state(prim, dim)
     if out is None:
         out = _alloc(dim + 1, n, prec, prim[0].device)
-    outs, _, _ = _planes(out, "prim2cons out", n, prec)
-    N.check(N.lib().fvb_prim2cons(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins),
-                                  N.ptr_array(outs), _stream(stream)))
+    outs, _, _ = _planes(out, "prim2cons out", n, prec, device=prim[0].device)
+    with torch.cuda.device(prim[0].device):
+        N.check(N.lib().fvb_prim2cons(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins),
+                                      N.ptr_array(outs), _stream(stream, prim[0].device)))
     return out
 
 
@@ -156,8 +183,10 @@ def v_mag2(state, dim, out=None, stream=None):
     ins, n, prec = _state(state, dim)
     if out is None:
         out = _alloc(1, n, prec, state[0].device)[0]
-    outs, _, _ = _planes([out], "v_mag2 out", n, prec)
-    N.check(N.lib().fvb_v_mag2(dim, prec, n, N.ptr_array(ins), outs[0], _stream(stream)))
+    outs, _, _ = _planes([out], "v_mag2 out", n, prec, device=state[0].device)
+    with torch.cuda.device(state[0].device):
+        N.check(N.lib().fvb_v_mag2(dim, prec, n, N.ptr_array(ins), outs[0],
+                                   _stream(stream, state[0].device)))
     return out
 
 
@@ -168,9 +197,10 @@ def eos(rho, e, p=None, T=None, gas=None, stream=None):
         p = _alloc(1, n, prec, rho.device)[0]
     if T is None:
         T = _alloc(1, n, prec, rho.device)[0]
-    outs, _, _ = _planes([p, T], "eos out", n, prec)
-    N.check(N.lib().fvb_eos(_gas_ptr(gas), prec, n, ins[0], ins[1], outs[0], outs[1],
-                            _stream(stream)))
+    outs, _, _ = _planes([p, T], "eos out", n, prec, device=rho.device)
+    with torch.cuda.device(rho.device):
+        N.check(N.lib().fvb_eos(_gas_ptr(gas), prec, n, ins[0], ins[1], outs[0], outs[1],
+                                _stream(stream, rho.device)))
     return p, T
 
 
@@ -181,15 +211,16 @@ def jacobian(state, dim, out=None, lambda_max=True, gas=None, stream=None):
     w = dim + 2
     if out is None:
         out = _alloc(dim * w * w, n, prec, state[0].device)
-    outs, _, _ = _planes(out, "jacobian out", n, prec)
+    outs, _, _ = _planes(out, "jacobian out", n, prec, device=state[0].device)
     lam = None
     if lambda_max is True:
         lam = torch.empty((), dtype=_DTYPE[prec], device=state[0].device)
-    elif isinstance(lambda_max, torch.Tensor):
+    elif lambda_max is not None and lambda_max is not False:
         lam = lambda_max
-    N.check(N.lib().fvb_jacobian(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins),
-                                 N.ptr_array(outs), lam.data_ptr() if lam is not None else None,
-                                 _stream(stream)))
+    lp = _scalar_out(lam, prec, state[0].device, "lambda_max") if lam is not None else None
+    with torch.cuda.device(state[0].device):
+        N.check(N.lib().fvb_jacobian(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins),
+                                     N.ptr_array(outs), lp, _stream(stream, state[0].device)))
     return out, lam
 
 
@@ -200,9 +231,12 @@ def wave_speed_max(state, dim, lam_out=None, lambda_max=None, gas=None, stream=N
         lambda_max = torch.empty((), dtype=_DTYPE[prec], device=state[0].device)
     lp = None
     if lam_out is not None:
-        lp = _planes([lam_out], "lambda out", n, prec)[0][0]
-    N.check(N.lib().fvb_wave_speed_max(_gas_ptr(gas), dim, prec, n, N.ptr_array(ins), lp,
-                                       lambda_max.data_ptr(), _stream(stream)))
+        lp = _planes([lam_out], "lambda out", n, prec, device=state[0].device)[0][0]
+    with torch.cuda.device(state[0].device):
+        N.check(N.lib().fvb_wave_speed_max(
+            _gas_ptr(gas), dim, prec, n, N.ptr_array(ins), lp,
+            _scalar_out(lambda_max, prec, state[0].device, "lambda_max"),
+            _stream(stream, state[0].device)))
     return lam_out, lambda_max
 
 
@@ -219,21 +253,25 @@ def csr_matvec_acc(row_ptr, col_idx, values, x, y, stream=None):
     if not values.is_cuda or values.dtype != torch.float64 or values.numel() != col_idx.numel():
         raise N.ArgumentError(N.FVB_EARG, "values must be float64 with one entry per index")
     (xp,), cols, px = _planes([x], "x")
-    (yp,), rows, py = _planes([y], "y")
+    (yp,), rows, py = _planes([y], "y", device=x.device)
     if row_ptr.numel() != rows + 1:
         raise N.LengthMismatch(N.FVB_ELEN, f"row_ptr has {row_ptr.numel()} entries for "
                                            f"{rows} rows")
+    if any(t.device != y.device for t in (row_ptr, col_idx, values)):
+        raise N.ArgumentError(N.FVB_EARG, "CSR arrays must be on the planes' device")
     fn = N.lib().fvb_csr_matvec_acc_u32 if col_idx.dtype == torch.int32 else \
         N.lib().fvb_csr_matvec_acc
-    N.check(fn(py, px, rows, col_idx.numel(), row_ptr.data_ptr(), col_idx.data_ptr(),
-               values.data_ptr(), xp, yp, _stream(stream)))
+    with torch.cuda.device(y.device):
+        N.check(fn(py, px, rows, col_idx.numel(), row_ptr.data_ptr(), col_idx.data_ptr(),
+                   values.data_ptr(), xp, yp, _stream(stream, y.device)))
     return y
 
 
 def axpy_sin(x, y, stream=None):
     """y <- 0.5*sin(x+y) in place."""
     ptrs, n, prec = _planes([x, y], "axpy_sin")
-    N.check(N.lib().fvb_axpy_sin(prec, n, ptrs[0], ptrs[1], _stream(stream)))
+    with torch.cuda.device(y.device):
+        N.check(N.lib().fvb_axpy_sin(prec, n, ptrs[0], ptrs[1], _stream(stream, y.device)))
     return y
 
 
@@ -242,8 +280,9 @@ def synth_state(dim, n, prec=1, seed=0x5EED, first=0, out=None, device="cuda", s
     if out is None:
         out = _alloc(dim + 2, n, prec, device)
     outs, _, p = _planes(out, "synth out", n, None) if n else ([0] * (dim + 2), 0, prec)
-    N.check(N.lib().fvb_synth_state(dim, prec, seed, first, n, N.ptr_array(outs),
-                                    _stream(stream)))
+    with torch.cuda.device(out[0].device if n else device):
+        N.check(N.lib().fvb_synth_state(dim, prec, seed, first, n, N.ptr_array(outs),
+                                        _stream(stream, out[0].device if n else device)))
     return out
 
 
@@ -253,7 +292,9 @@ def synth_uniform(n, prec=1, seed=1, first=0, lo=0.25, hi=4.0, out=None, device=
     if out is None:
         out = _alloc(1, n, prec, device)[0]
     ptr = out.data_ptr() if n else None
-    N.check(N.lib().fvb_synth_uniform(prec, seed, first, n, lo, hi, ptr, _stream(stream)))
+    with torch.cuda.device(out.device):
+        N.check(N.lib().fvb_synth_uniform(prec, seed, first, n, lo, hi, ptr,
+                                          _stream(stream, out.device)))
     return out
 
 

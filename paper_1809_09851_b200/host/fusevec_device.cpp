@@ -336,7 +336,18 @@ struct HostCopies {
             std::size_t base = 0;
             for (const HostWrite& j : jobs) {
                 const std::size_t b = j.dst->byte_size();
-                const std::size_t a = std::max(lo, base), e = std::min(hi, base + b);
+                // the thread boundaries, rounded down to whole elements of
+                // this job relative to its own start: neighbouring threads
+                // round the shared boundary alike, so the pieces still tile
+                // the job, and every piece starts element-aligned (jobs of
+                // mixed precisions put f64 jobs at 4 mod 8 of the range)
+                if (hi <= base || lo >= base + b) {
+                    base += b;
+                    continue;
+                }
+                const std::size_t w = j.dst->precision() == Precision::f64 ? 8 : 4;
+                const std::size_t a = base + ((std::max(lo, base) - base) & ~(w - 1));
+                const std::size_t e = base + ((std::min(hi, base + b) - base) & ~(w - 1));
                 char* d = static_cast<char*>(j.dst->raw()) + (a - base);
                 if (a < e && j.src) {
                     std::memcpy(d, static_cast<const char*>(j.src->raw()) + (a - base), e - a);
@@ -771,7 +782,17 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
     // reading a vector an earlier item of the same block wrote sees the new
     // values; one fused pass reads every operand before writing anything.
     // Such blocks are evaluated item by item instead, in the reference's order.
-    const bool hazard = reads_earlier_destination(be, items, outs, matvecs);
+    bool hazard = reads_earlier_destination(be, items, outs, matvecs);
+    // Two items writing one destination: the later one's value stands, as
+    // item-by-item evaluation leaves it (the host-buffer pipeline refuses
+    // one plane named for two outputs).
+    if (!hazard && !need_reduce && matvecs.empty()) {
+        std::unordered_map<const void*, int> seen;
+        for (const Out& o : outs)
+            if ((o.host || o.dev) &&
+                ++seen[o.host ? static_cast<const void*>(o.host) : o.dev] > 1)
+                hazard = true;
+    }
     if (hazard && (need_reduce || !matvecs.empty()))
         throw UnsupportedExpression(
             "block whose destinations alias operands of its own items (CFL or matvec block)");
@@ -814,8 +835,26 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
                 rest_outs.push_back(outs[i]);
             }
         }
+        // The stripped copies run after the kernel.  The reference copies
+        // each one at its own position (block.cpp:413-451), so a later item
+        // that overwrites a copy's source -- e.g. convert(u, Primitive) with
+        // the pressure written over rho -- must not run first: such blocks
+        // keep the bare-leaf items inside the fused pass, which reads every
+        // leaf before it writes.  So must blocks where a computed item and a
+        // copy name one destination.
+        auto overwrites_a_source = [&] {
+            for (const auto& [src, o] : stripped) {
+                const DeviceVector* rs = be.residency ? be.residency->find(src) : nullptr;
+                for (const Out& r : rest_outs) {
+                    if ((r.host && r.host == src) || (r.dev && rs && r.dev == rs)) return true;
+                    // one destination for both: the later item's value wins
+                    if ((r.host && r.host == o.host) || (r.dev && r.dev == o.dev)) return true;
+                }
+            }
+            return false;
+        };
         Plan alt;
-        if (!stripped.empty() && !rest.empty() &&
+        if (!stripped.empty() && !rest.empty() && !overwrites_a_source() &&
             try_plan(rest, rest_outs, rest.size(), 1, &alt) && (!alt.k.impl || !whole)) {
             plan = std::move(alt);
             copies = std::move(stripped);

@@ -997,6 +997,89 @@ void run_gpu() {
         return "";
     });
 
+    check("a later item overwriting a pass-through's source: convert with p written over rho", [&] {
+        // convert(u, Primitive).block() = [rho, v.., p]: the fused kernel
+        // covers the computed items and rho is a plain copy.  With p's
+        // destination = the rho leaf itself, the reference copies rho at
+        // item 0, before item d+1 overwrites it (block.cpp:413-451); the
+        // copy must not run after the kernel.  Host leaves (staged path) and
+        // resident leaves (device path, tie'd outputs) both.
+        SplitMix64 rng(0xD4);
+        for (std::size_t d = 1; d <= 3; ++d) {
+            const std::size_t n = 5003;
+            auto f = random_state(d, n, rng);
+            // the grid's last item holds rho: p is written over its own leaf
+            auto column = [&] {
+                std::vector<DenseVector> c;
+                for (std::size_t i = 0; i + 1 < d + 2; ++i) c.emplace_back(Precision::f64, n);
+                c.push_back(f[0]);
+                return BlockColVector(std::move(c));
+            };
+            auto state = [&](BlockColVector& col) {
+                std::vector<Expr> lv{leaf(col.get(d + 1))};
+                for (std::size_t i = 1; i < d + 2; ++i) lv.push_back(leaf(f[i]));
+                return state_conservative(EosSpec(), d, lv);
+            };
+            BlockColVector want = column(), got = column();
+            StateSet uw = state(want), ug = state(got);
+            evaluate_block(ref, convert(uw, Formulation::Primitive).block(), want);
+            dev::evaluate_block(be, convert(ug, Formulation::Primitive).block(), got);
+            for (std::size_t i = 0; i < d + 2; ++i)
+                if (!same_bits(want.get(i), got.get(i)))
+                    fail("d=" + std::to_string(d) + " host item " + std::to_string(i));
+            if (!same_bits(want.get(0), f[0])) fail("the reference's copy is not the old rho");
+            // resident: every leaf bound, p tie'd over rho's resident plane
+            BlockColVector rcol = column();
+            StateSet ur = state(rcol);
+            std::vector<dev::DeviceVector> planes;
+            dev::Residency res;
+            std::vector<const DenseVector*> hosts{&rcol.get(d + 1)};
+            for (std::size_t i = 1; i < d + 2; ++i) hosts.push_back(&f[i]);
+            for (const DenseVector* h : hosts) {
+                planes.push_back(dev::make_temp(Precision::f64, n));
+                planes.back().upload(*h);
+            }
+            for (std::size_t i = 0; i < hosts.size(); ++i) res.bind(*hosts[i], planes[i]);
+            dev::DeviceBackend rb = be;
+            rb.residency = &res;
+            std::vector<dev::DeviceVector> outs;
+            for (std::size_t i = 0; i + 1 < d + 2; ++i) outs.push_back(dev::make_temp(Precision::f64, n));
+            dev::Tie t;
+            for (auto& o : outs) t.dests.push_back(&o);
+            t.dests.push_back(&planes[0]);
+            dev::evaluate_block(rb, convert(ur, Formulation::Primitive).block(), t);
+            DenseVector tmp(Precision::f64, n);
+            for (std::size_t i = 0; i < d + 2; ++i) {
+                (i + 1 < d + 2 ? outs[i] : planes[0]).download(tmp);
+                if (!same_bits(want.get(i), tmp))
+                    fail("d=" + std::to_string(d) + " resident item " + std::to_string(i));
+            }
+        }
+        return "";
+    });
+
+    check("two items naming one destination: the later item's value stands", [&] {
+        // tie(X, v.., X) for convert(u, Primitive).block(): item 0 copies rho
+        // into X, item d+1 then writes p there (the reference's item order).
+        SplitMix64 rng(0xD5);
+        for (std::size_t d = 1; d <= 3; ++d) {
+            const std::size_t n = 4099;
+            auto f = random_state(d, n, rng);
+            StateSet u = state_conservative(EosSpec(), d, leaves_of(f));
+            std::vector<dev::DeviceVector> outs;
+            for (std::size_t i = 0; i < d + 1; ++i) outs.push_back(dev::make_temp(Precision::f64, n));
+            dev::Tie t;
+            for (auto& o : outs) t.dests.push_back(&o);
+            t.dests.push_back(&outs[0]);
+            dev::evaluate_block(be, convert(u, Formulation::Primitive).block(), t);
+            DenseVector want(Precision::f64, n), got(Precision::f64, n);
+            evaluate(ref, derived_p(u), want);
+            outs[0].download(got);
+            if (!same_bits(want, got)) fail("d=" + std::to_string(d) + ": X is not p");
+        }
+        return "";
+    });
+
     check("in place through a hand-written kernel: pressure into rhoE (d=3)", [&] {
         SplitMix64 rng(0xC3);
         const std::size_t n = 70000;

@@ -211,6 +211,34 @@ def test_lambda_max_exact_and_nan(cuda, orc):
     assert lam.item() == 0.0
 
 
+def test_lambda_max_output_is_validated(cuda, orc):
+    # the caller's accumulator must be one element of the state's precision on
+    # the state's device: anything else would be an out-of-bounds or foreign
+    # device write (memset + atomicMax of sizeof(T) bytes)
+    s = fvb.synth_state(3, 1000, prec=1)
+    for bad, err in [(torch.empty((), dtype=torch.float32, device=cuda), fvb.PrecisionError),
+                     (torch.empty((), dtype=torch.float64), fvb.ArgumentError),
+                     (torch.empty(0, dtype=torch.float64, device=cuda), fvb.ArgumentError)]:
+        with pytest.raises(err):
+            fvb.jacobian(s, 3, lambda_max=bad)
+        with pytest.raises(err):
+            fvb.wave_speed_max(s, 3, lambda_max=bad)
+    # a refused call enqueues nothing: the caller's word keeps its value
+    lam = torch.full((), 7.0, dtype=torch.float64, device=cuda)
+    outs = [torch.empty(1000, dtype=torch.float64, device=cuda) for _ in range(75)]
+    raw = torch.empty(1001 * 8, dtype=torch.uint8, device=cuda)
+    odd = raw[4:4 + 1000 * 8].view(torch.float32)  # a misaligned f64 plane, by pointer
+    args = [t.data_ptr() for t in s]
+    args[2] = odd.data_ptr()
+    for fn, extra in [(N.lib().fvb_jacobian, [N.ptr_array([t.data_ptr() for t in outs])]),
+                      (N.lib().fvb_wave_speed_max, [None])]:
+        with pytest.raises(fvb.ArgumentError):
+            N.check(fn(None, 3, 1, 1000, N.ptr_array(args), *extra, lam.data_ptr(),
+                       torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        assert lam.item() == 7.0
+
+
 def test_lambda_invariant_to_slicing(cuda, orc):
     # Shard the range like the multi-GPU path; the max over slice maxima is
     # bitwise the global max (order-independent reduction).
@@ -338,6 +366,42 @@ def test_host_path_matches_device(cuda, orc, pinned):
     assert lam == lam_np
     # all 75, the 30 constant entries filled host-side included
     assert all_same([t.numpy() for t in jo], j_np)
+    ctx.close()
+
+
+@pytest.mark.parametrize("outputs", ["device", "reduce_only"])
+def test_host_path_pageable_inputs_busy_stream(cuda, orc, outputs):
+    # Pageable inputs bounce through the slot's pinned buffer; chunk c+3 is
+    # packed into the buffer chunk c used.  With device (or no) outputs no
+    # unpack waits on the slot, and with the `after` stream still busy every
+    # H2D is queued behind it -- the packing must wait for chunk c's copies
+    # anyway, else chunk c computes on chunk c+3's data.
+    dim, n = 3, 1_000_003
+    s_np = orc.random_state(dim, n, seed=21)
+    ctx = fvb.HostContext(0, chunk_points=1 << 13)  # 123 chunks
+    k = _flux_kernel() if outputs == "device" else None
+    busy = torch.cuda.Stream()
+    with torch.cuda.stream(busy):
+        torch.cuda._sleep(400_000_000)  # ~0.2 s of queued work ahead of the pipeline
+    if outputs == "device":
+        leaves = [None] * k.n_inputs
+        for ci in range(k.n_inputs):
+            leaves[k.in_slot[ci]] = torch.from_numpy(s_np[ci])
+        outs = [torch.empty(n, dtype=torch.float64, device=cuda) for _ in range(15)]
+        ctx.launch(k, outs + leaves, n, after=busy)
+        assert all_same([t.cpu().numpy() for t in outs], orc.flux(dim, s_np))
+    else:
+        import re
+        import struct
+        pat = dict(fvb.patterns())["wave_speed3_f64"]
+        kw = fvb.lookup(re.sub(r"Cd#(\w+);", lambda m: "Cd%016x;" % struct.unpack(
+            "<Q", struct.pack("<d", {"half": 0.5, "gm1": 0.4, "gamma": 1.4}[m.group(1)]))[0],
+            pat))
+        lv = [None] * kw.n_inputs
+        for ci in range(kw.n_inputs):
+            lv[kw.in_slot[ci]] = torch.from_numpy(s_np[ci])
+        lam = ctx.launch(kw, [None] + lv, n, reduce=True, after=busy)
+        assert lam == orc.wave_speed_max(dim, s_np)
     ctx.close()
 
 
