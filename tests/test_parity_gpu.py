@@ -422,6 +422,47 @@ def test_host_path_rejects_one_plane_for_two_outputs(cuda, orc):
     ctx.close()
 
 
+def test_host_path_refuses_device_planes_before_host_threads(cuda, orc):
+    # the raw C ABI handed device pointers as host planes: refused with
+    # FVB_EARG before any host thread touches them (the pass-through rows,
+    # the Jacobian's constant fills), not a wild host access
+    n = 4096
+    s = [t for t in fvb.synth_state(3, n, prec=1)]
+    ctx = fvb.HostContext(0)
+    hs = [torch.empty(n, dtype=torch.float64) for _ in range(5)]
+    for ins, outs, count in (
+        (s, [torch.empty(n, dtype=torch.float64) for _ in range(15)], 15),       # device inputs
+        (hs, [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(15)], 15),
+    ):
+        st = N.lib().fvb_flux_host(ctx._h, None, 3, 1, n, N.ptr_array([t.data_ptr() for t in ins]),
+                                   N.ptr_array([t.data_ptr() for t in outs]))
+        assert st == N.FVB_EARG and b"device memory" in N.lib().fvb_last_error()
+    jo = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(75)]
+    lam = ctypes.c_double()
+    st = N.lib().fvb_jacobian_host(ctx._h, None, 3, 1, n, N.ptr_array([t.data_ptr() for t in hs]),
+                                   N.ptr_array([t.data_ptr() for t in jo]), ctypes.byref(lam))
+    assert st == N.FVB_EARG and b"device memory" in N.lib().fvb_last_error()
+    # fvb_launch_host: a device plane flagged as host (arg_on_device 0)
+    import re
+    import struct
+    pat = dict(fvb.patterns())["pressure3_f64"]
+    kp = fvb.lookup(re.sub(r"Cd#(\w+);", lambda m: "Cd%016x;" % struct.unpack(
+        "<Q", struct.pack("<d", {"half": 0.5, "gm1": 0.4}[m.group(1)]))[0], pat))
+    count = 1 + kp.n_inputs
+    for ptrs in ([jo[0].data_ptr()] + [t.data_ptr() for t in hs[:kp.n_inputs]],
+                 [hs[0].data_ptr()] + [t.data_ptr() for t in s[:kp.n_inputs]]):
+        st = N.lib().fvb_launch_host(ctx._h, ctypes.byref(kp), n, N.ptr_array(ptrs),
+                                     (ctypes.c_uint8 * count)(*([1] * count)),
+                                     (ctypes.c_uint8 * count)(*([0] * count)), None, None)
+        assert st == N.FVB_EARG and b"device memory" in N.lib().fvb_last_error()
+    # the context still works afterwards
+    s_np = orc.random_state(3, n, seed=11)
+    fo = [torch.empty(n, dtype=torch.float64) for _ in range(15)]
+    ctx.flux([torch.from_numpy(a) for a in s_np], 3, fo)
+    assert all(a.numpy().tobytes() == b.tobytes() for a, b in zip(fo, orc.flux(3, s_np)))
+    ctx.close()
+
+
 @pytest.mark.parametrize("prec", ["f64", "f32"])
 def test_host_jacobian_constant_fills(cuda, orc, prec):
     # the constant entries (0, 1, gamma-1) are filled by host threads: every
