@@ -58,7 +58,10 @@ class CopyPool {
     // Every piece copied when this returns; the calling thread helps.
     void run(const std::vector<Piece>& pieces) {
         if (pieces.empty()) return;
-        if (threads_.empty() || pieces.size() == 1) {
+        size_t total = 0;
+        for (const Piece& p : pieces) total += p.bytes;
+        // waking the workers costs more than copying a few hundred KiB
+        if (threads_.empty() || pieces.size() == 1 || total < (size_t(1) << 20)) {
             for (const Piece& p : pieces) host_copy(p.dst, p.src, p.bytes);
             return;
         }
@@ -444,8 +447,11 @@ struct HostSide {
     HostSide(const std::vector<HostJob>& jobs, size_t bytes) {
         if (jobs.empty() || bytes == 0) return;
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-        const unsigned nt = std::min(8u, std::max(1u, hw / 2));
         const size_t total = jobs.size() * bytes;
+        // a thread per 1 MiB at most: a thread costs tens of microseconds to
+        // start and join, so a small call writes inline (below)
+        const unsigned nt = unsigned(std::min<size_t>(std::min(8u, std::max(1u, hw / 2)),
+                                                      std::max<size_t>(1, total >> 20)));
         const size_t per = ((total + nt - 1) / nt + 63) & ~size_t(63);  // whole elements
         auto work = [jobs, bytes](size_t lo, size_t hi) {
             while (lo < hi) {
@@ -459,6 +465,10 @@ struct HostSide {
                 lo += len;
             }
         };
+        if (nt == 1) {
+            work(0, total);
+            return;
+        }
         try {
             for (unsigned t = 0; t < nt && size_t(t) * per < total; ++t) {
                 const size_t lo = size_t(t) * per;

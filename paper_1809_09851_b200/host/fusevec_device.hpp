@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "fusevec/backend.hpp"
+#include "fusevec/bench.hpp"
 #include "fusevec/block.hpp"
 #include "fusevec/dense_vector.hpp"
 #include "fusevec/error.hpp"
@@ -125,6 +126,10 @@ class DeviceCsr {
 
 class Residency {
   public:
+    Residency();
+    Residency(const Residency& o);
+    Residency& operator=(const Residency& o);
+
     void bind(const DenseVector& host, DeviceVector& dev);
     void unbind(const DenseVector& host);
     DeviceVector* find(const DenseVector* host) const;
@@ -133,9 +138,15 @@ class Residency {
     void unbind(const SparseMatrix& host);
     DeviceCsr* find(const SparseMatrix* host) const;
 
+    /// Changes with every bind / unbind and is unique per object (copies
+    /// get their own): evaluations that reuse one block expression key
+    /// their cached launch plan on it.
+    std::uint64_t version() const { return version_; }
+
   private:
     std::unordered_map<const DenseVector*, DeviceVector*> map_;
     std::unordered_map<const SparseMatrix*, DeviceCsr*> csr_;
+    std::uint64_t version_;
 };
 
 /// Evaluation strategy for the device path (the analog of Backend).
@@ -203,6 +214,29 @@ double evaluate_block_cfl(const DeviceBackend& be, const BlockExpr& jacobian, co
 /// a CUDA graph and the maximum consumed by later device work.
 void evaluate_block_cfl(const DeviceBackend& be, const BlockExpr& jacobian, const Tie& dest,
                         DeviceVector& lambda_max);
+
+// ---- the reference's benchmark harness on the device (fusevec_device_bench.cpp) ----
+
+/// Where the benchmark's planes live: device-resident (leaves bound through
+/// a Residency, outputs DeviceVectors / a Tie) or the reference's own host
+/// DenseVectors (staged over PCIe on every call).
+enum class BenchPlanes { Device, Host };
+
+/// Backend label of device records: "b200x<G>" (G = ordinals, at least 1).
+std::string bench_label(const DeviceBackend& be);
+
+/// proj/include/fusevec/bench.hpp run_micro / run_miniapp with the device
+/// backend: cfg's suite, sizes, reps, precision as the reference reads them
+/// (cfg.backend is ignored: `be` evaluates).  Records carry the same fields;
+/// overhead_ratio = the reference-API call (evaluate / evaluate_block of the
+/// reference's tree) over the fused kernel called directly through the C ABI.
+/// Throws OracleMismatch if either differs from the other or from the
+/// reference's Backend::scalar_ref() in one bit.  write_csv (bench.hpp)
+/// writes the records in the reference's CSV schema.
+std::vector<BenchRecord> run_micro(const BenchConfig& cfg, const DeviceBackend& be,
+                                   BenchPlanes where = BenchPlanes::Device);
+std::vector<BenchRecord> run_miniapp(const BenchConfig& cfg, const DeviceBackend& be,
+                                     BenchPlanes where = BenchPlanes::Device);
 
 }  // namespace device
 }  // namespace fusevec

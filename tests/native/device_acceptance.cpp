@@ -938,6 +938,92 @@ void run_gpu() {
         return "";
     });
 
+    check("a reused block expression (launch-plan cache) follows new data, residency and vector changes", [&] {
+        SplitMix64 rng(34);
+        const std::size_t n = 4099;
+        auto f = random_state(3, n, rng);
+        StateSet u = state_conservative(EosSpec(), 3, leaves_of(f));
+        const BlockExpr F = inviscid_flux(u);  // built once, evaluated many times
+        std::vector<dev::DeviceVector> planes;
+        dev::Residency res;
+        for (auto& v : f) {
+            planes.push_back(dev::make_temp(Precision::f64, n));
+            planes.back().upload(v);
+        }
+        for (std::size_t i = 0; i < 5; ++i) res.bind(f[i], planes[i]);
+        dev::DeviceBackend rb;
+        rb.residency = &res;
+        std::vector<dev::DeviceVector> out;
+        for (int i = 0; i < 15; ++i) out.push_back(dev::make_temp(Precision::f64, n));
+        dev::Tie t;
+        for (auto& o : out) t.dests.push_back(&o);
+        DenseVector tmp(Precision::f64, n);
+        auto agree = [&](const char* what) {
+            BlockVectorGrid want(5, 3, Precision::f64, n);
+            evaluate_block(ref, F, want);
+            for (std::size_t i = 0; i < 15; ++i) {
+                out[i].download(tmp);
+                if (!same_bits(tmp, want.get(i)))
+                    fail(std::string(what) + ": item " + std::to_string(i));
+            }
+        };
+        dev::evaluate_block(rb, F, t);
+        dev::evaluate_block(rb, F, t);  // the cached plan
+        agree("second call");
+        // new state values (in place on host and device): the plan holds no data
+        auto g = random_state(3, n, rng);
+        for (std::size_t i = 0; i < 5; ++i) {
+            std::memcpy(f[i].raw(), g[i].raw(), f[i].byte_size());
+            planes[i].upload(f[i]);
+        }
+        dev::evaluate_block(rb, F, t);
+        agree("new data");
+        // unbind rhoE and change it on the host only: the evaluation must read
+        // the host vector now, not the stale resident plane
+        res.unbind(f[4]);
+        const DenseVector saved = f[4];
+        for (std::size_t i = 0; i < n; ++i) f[4].set(i, f[4].at(i) * 1.5);
+        dev::evaluate_block(rb, F, t);
+        agree("after unbind");
+        res.bind(f[4], planes[4]);  // bound again: the (older) resident plane is read
+        dev::evaluate_block(rb, F, t);
+        std::memcpy(f[4].raw(), saved.raw(), f[4].byte_size());  // what the plane holds
+        agree("after re-bind");
+        // other destinations: a host grid, then another one
+        BlockVectorGrid g1(5, 3, Precision::f64, n), g2(5, 3, Precision::f64, n), want(5, 3, Precision::f64, n);
+        dev::evaluate_block(rb, F, g1);
+        dev::evaluate_block(rb, F, g2);
+        evaluate_block(ref, F, want);
+        for (std::size_t i = 0; i < 15; ++i)
+            if (!same_bits(g1.get(i), want.get(i)) || !same_bits(g2.get(i), want.get(i)))
+                fail("host grids: item " + std::to_string(i));
+        // single expressions reuse their plan the same way
+        const Expr P = derived_p(u);
+        DenseVector p1(Precision::f64, n), pw(Precision::f64, n);
+        dev::evaluate(rb, P, p1);
+        dev::evaluate(rb, P, p1);
+        evaluate(ref, P, pw);
+        if (!same_bits(p1, pw)) fail("cached evaluate");
+        // a leaf reassigned to another length: refused, not served from the cache
+        dev::DeviceBackend hb;  // no residency: host leaves
+        dev::evaluate_block(hb, F, g1);
+        dev::evaluate(hb, P, p1);
+        f[2] = DenseVector(Precision::f64, n + 1);
+        int refused = 0;
+        try {
+            dev::evaluate_block(hb, F, g1);
+        } catch (const LengthMismatch&) {
+            ++refused;
+        }
+        try {
+            dev::evaluate(hb, P, p1);
+        } catch (const LengthMismatch&) {
+            ++refused;
+        }
+        if (refused != 2) fail("a resized leaf was not refused");
+        return "";
+    });
+
     check("aliased pass-through: flux into a grid whose row 0 is the momentum fields", [&] {
         // proj/src/block.cpp:419-422 skips an item whose destination is its
         // own bare leaf; the remaining items are still fused into one pass.

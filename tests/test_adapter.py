@@ -30,7 +30,7 @@ def test_reference_trees_resolve_to_fused_kernels():
 @pytest.mark.gpu
 def test_reference_api_on_device(cuda):
     out = run("gpu")
-    assert out.count("[PASS]") == 25
+    assert out.count("[PASS]") == 26
 
 
 @pytest.mark.gpu
@@ -40,7 +40,7 @@ def test_reference_api_on_device_all_lowered(cuda, monkeypatch):
     # hand-written kernels: still bitwise against the reference engine.
     monkeypatch.setenv("FVB_FORCE_LOWER", "1")
     out = run("gpu")
-    assert out.count("[PASS]") == 25
+    assert out.count("[PASS]") == 26
 
 
 def test_adapter_compiles_in_the_references_own_namespace():
@@ -49,8 +49,51 @@ def test_adapter_compiles_in_the_references_own_namespace():
     inc = "/root/reference/proj/include"
     if not os.path.isdir(inc):
         pytest.skip("reference headers not mounted")
-    src = os.path.join(ROOT, "paper_1809_09851_b200", "host", "fusevec_device.cpp")
-    p = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Werror", f"-I{inc}",
-                        f"-I{ROOT}/include", f"-I{ROOT}/paper_1809_09851_b200/host",
-                        "-I/usr/local/cuda/include", src], capture_output=True, text=True)
-    assert p.returncode == 0, p.stderr
+    for name in ("fusevec_device.cpp", "fusevec_device_bench.cpp"):
+        src = os.path.join(ROOT, "paper_1809_09851_b200", "host", name)
+        p = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Werror", f"-I{inc}",
+                            f"-I{ROOT}/include", f"-I{ROOT}/paper_1809_09851_b200/host",
+                            "-I/usr/local/cuda/include", src], capture_output=True, text=True)
+        assert p.returncode == 0, (name, p.stderr)
+
+
+BENCH = os.path.join(ROOT, "tests", "native", "build", "device_bench")
+CSV_HEADER = "suite,backend,precision,n,median_ns,mflops,bandwidth_mbs,overhead_ratio"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", ["micro", "miniapp"])
+@pytest.mark.parametrize("planes", ["device", "host"])
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_reference_bench_suites_on_device(cuda, tmp_path, suite, planes, prec):
+    # the reference's harness (run_micro / run_miniapp, bench.cpp) through the
+    # reference's API on the device: it throws OracleMismatch unless the
+    # generic call, the direct C-ABI call and the reference's scalar_ref agree
+    # bit for bit at every size; the CSV is the reference's write_csv
+    if not os.path.exists(BENCH):
+        pytest.skip("tests/native/build/device_bench not built")
+    csv = tmp_path / "out.csv"
+    p = subprocess.run([BENCH, suite, "--sizes", "1000,4096,70001", "--reps", "5",
+                        "--precision", prec, "--planes", planes, "--csv", str(csv)],
+                       capture_output=True, text=True, timeout=600)
+    print(p.stdout, p.stderr)
+    assert p.returncode == 0, p.stdout + p.stderr
+    lines = csv.read_text().splitlines()
+    assert lines[0].startswith("# micro accounting") and lines[2] == CSV_HEADER
+    rows = [ln.split(",") for ln in lines[3:]]
+    assert [int(r[3]) for r in rows] == [1000, 4096, 70001]
+    label = "b200x1" + ("-host" if planes == "host" else "")
+    for r in rows:
+        assert r[0] == suite and r[1] == label and r[2] == prec
+        med, mflops, mbs, ratio = map(float, r[4:])
+        assert med > 0 and mflops > 0 and mbs > 0 and 0 < ratio < 100
+
+
+@pytest.mark.gpu
+def test_reference_bench_rejects_bad_config(cuda):
+    if not os.path.exists(BENCH):
+        pytest.skip("tests/native/build/device_bench not built")
+    # BenchConfig::validate (bench.cpp:106-115): sizes strictly increasing
+    p = subprocess.run([BENCH, "micro", "--sizes", "4096,1024"], capture_output=True, text=True,
+                       timeout=120)
+    assert p.returncode == 1 and "increasing" in p.stderr
