@@ -224,6 +224,31 @@ void run_gpu() {
     dev::DeviceBackend be;
     Backend ref = Backend::scalar_ref();
 
+    check("criterion 1 on device: zero overhead, the reference's gate (acceptance.cpp:46-62)", [&] {
+        // run_micro at n = 2^20, auto reps: the reference's tree through
+        // evaluate() against the fused kernel called directly; the harness
+        // itself checks both against scalar_ref bit for bit
+        const double gate = 1.10;
+        double ratio[2], mini[2];
+        const Precision precs[2] = {Precision::f64, Precision::f32};
+        for (int k = 0; k < 2; ++k) {
+            BenchConfig cfg;
+            cfg.sizes = {1u << 20};
+            cfg.reps = 0;
+            cfg.precision = precs[k];
+            cfg.suite = "micro";
+            ratio[k] = dev::run_micro(cfg, be).at(0).overhead_ratio;
+            cfg.suite = "miniapp";
+            mini[k] = dev::run_miniapp(cfg, be).at(0).overhead_ratio;
+        }
+        char buf[200];
+        std::snprintf(buf, sizeof buf,
+                      "n=2^20 micro ratios f64 %.4f, f32 %.4f (gate %.2f); miniapp f64 %.4f, f32 %.4f",
+                      ratio[0], ratio[1], gate, mini[0], mini[1]);
+        if (ratio[0] > gate || ratio[1] > gate) fail(buf);
+        return std::string(buf);
+    });
+
     check("general lowering: random trees (the reference's TreeGen) vs scalar_ref", [&] {
         // proj/tests/test_backend.cpp:267-290 checks its compiled path on
         // TreeGen trees at n=16384; here the device path (fvb_lookup's NVRTC
