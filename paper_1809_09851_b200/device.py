@@ -119,6 +119,13 @@ def _planes(planes: Sequence[torch.Tensor], what: str, n: Optional[int] = None,
     return ptrs, n, prec
 
 
+def _count(planes, count: int, what: str) -> None:
+    """The C ABI reads exactly `count` plane pointers: a shorter list would
+    hand it pointers from past the end of the array."""
+    if len(planes) != count:
+        raise N.ArgumentError(N.FVB_EARG, f"{what}: {count} planes expected, got {len(planes)}")
+
+
 def _alloc(count: int, n: int, prec: int, device) -> list:
     return [torch.empty(n, dtype=_DTYPE[prec], device=device) for _ in range(count)]
 
@@ -133,6 +140,8 @@ def _state(state, dim):
 def flux(state: Sequence[torch.Tensor], dim: int, out=None, gas: Optional[Gas] = None,
          stream=None):
     """inviscid_flux of a conservative state: (d+2)*d planes, item r*d+c."""
+    if out is not None:
+        _count(out, (dim + 2) * dim, "flux out")
     ins, n, prec = _state(state, dim)
     if out is None:
         out = _alloc((dim + 2) * dim, n, prec, state[0].device)
@@ -145,6 +154,8 @@ def flux(state: Sequence[torch.Tensor], dim: int, out=None, gas: Optional[Gas] =
 
 def flux_prim(prim, dim, out=None, gas=None, stream=None):
     """inviscid_flux of a primitive state [rho, v.., p] (fluid.cpp:290-298)."""
+    if out is not None:
+        _count(out, (dim + 2) * dim, "flux_prim out")
     ins, n, prec = _state(prim, dim)
     if out is None:
         out = _alloc((dim + 2) * dim, n, prec, prim[0].device)
@@ -157,6 +168,8 @@ def flux_prim(prim, dim, out=None, gas=None, stream=None):
 
 def cons2prim(state, dim, out=None, gas=None, stream=None):
     """[v_0..v_{d-1}, p, c] of a conservative state."""
+    if out is not None:
+        _count(out, dim + 2, "cons2prim out")
     ins, n, prec = _state(state, dim)
     if out is None:
         out = _alloc(dim + 2, n, prec, state[0].device)
@@ -169,6 +182,8 @@ def cons2prim(state, dim, out=None, gas=None, stream=None):
 
 def prim2cons(prim, dim, out=None, gas=None, stream=None):
     """[m_0..m_{d-1}, rhoE] of a primitive state [rho, v.., p]."""
+    if out is not None:
+        _count(out, dim + 1, "prim2cons out")
     ins, n, prec = _state(prim, dim)
     if out is None:
         out = _alloc(dim + 1, n, prec, prim[0].device)
@@ -207,6 +222,8 @@ def eos(rho, e, p=None, T=None, gas=None, stream=None):
 def jacobian(state, dim, out=None, lambda_max=True, gas=None, stream=None):
     """Flux Jacobians [k][r][c] (d*(d+2)^2 planes) and, unless lambda_max is
     False, a 0-d device tensor holding the CFL max wave speed."""
+    if out is not None:
+        _count(out, dim * (dim + 2) ** 2, "jacobian out")
     ins, n, prec = _state(state, dim)
     w = dim + 2
     if out is None:
@@ -279,7 +296,9 @@ def synth_state(dim, n, prec=1, seed=0x5EED, first=0, out=None, device="cuda", s
     """random_state of acceptance.cpp:214-230 for global points [first, first+n)."""
     if out is None:
         out = _alloc(dim + 2, n, prec, device)
-    outs, _, p = _planes(out, "synth out", n, None) if n else ([0] * (dim + 2), 0, prec)
+    _count(out, dim + 2, "synth out")
+    # the generator writes planes of `prec`: their dtype and length must match
+    outs, _, _ = _planes(out, "synth out", n, prec) if n else ([0] * (dim + 2), 0, prec)
     with torch.cuda.device(out[0].device if n else device):
         N.check(N.lib().fvb_synth_state(dim, prec, seed, first, n, N.ptr_array(outs),
                                         _stream(stream, out[0].device if n else device)))
@@ -291,7 +310,7 @@ def synth_uniform(n, prec=1, seed=1, first=0, lo=0.25, hi=4.0, out=None, device=
     """make_vec of oracle.hpp:118-123: uniform(lo, hi) of draws [first, first+n)."""
     if out is None:
         out = _alloc(1, n, prec, device)[0]
-    ptr = out.data_ptr() if n else None
+    ptr = _planes([out], "synth_uniform out", n, prec)[0][0] if n else None
     with torch.cuda.device(out.device):
         N.check(N.lib().fvb_synth_uniform(prec, seed, first, n, lo, hi, ptr,
                                           _stream(stream, out.device)))
@@ -368,6 +387,8 @@ class HostContext:
         return ptrs, n, prec
 
     def flux(self, state, dim, out, gas=None):
+        _count(state, dim + 2, "state")
+        _count(out, (dim + 2) * dim, "flux out")
         ins, n, prec = self._host(state, "state")
         outs, _, _ = self._host(out, "out", n, prec)
         N.check(N.lib().fvb_flux_host(self._h, _gas_ptr(gas), dim, prec, n, N.ptr_array(ins),
@@ -403,6 +424,8 @@ class HostContext:
         return lam.value if reduce else None
 
     def jacobian(self, state, dim, out, gas=None):
+        _count(state, dim + 2, "state")
+        _count(out, dim * (dim + 2) ** 2, "jacobian out")
         ins, n, prec = self._host(state, "state")
         outs, _, _ = self._host(out, "out", n, prec)
         lam = ctypes.c_double()

@@ -61,8 +61,17 @@ def cfl_lambda_max(state, dim, gas=None, stream=None, group=None):
     """Global CFL wave speed of a sharded conservative state: the fused
     device reduction over this rank's slice (fvb_wave_speed_max), then the
     one NCCL all-reduce(MAX).  Returns a 0-d float64 device tensor."""
+    import torch
+
     from . import device
 
     _, lam = device.wave_speed_max(state, dim, gas=gas, stream=stream)
-    lam64 = lam.to(dtype=__import__("torch").float64)
+    if stream is not None:
+        # the reduction ran on the caller's stream: the widening copy and the
+        # all-reduce below run on the current one, so order them after it
+        if not isinstance(stream, torch.cuda.Stream):
+            stream = torch.cuda.ExternalStream(int(getattr(stream, "cuda_stream", stream)),
+                                               device=state[0].device)
+        torch.cuda.current_stream(state[0].device).wait_stream(stream)
+    lam64 = lam.to(dtype=torch.float64)
     return allreduce_max(lam64, group)

@@ -235,3 +235,27 @@ def test_lowered_images_are_cached_on_disk(tmp_path):
     assert _compile_in_subprocess({"FVB_CACHE_DIR": "off", "HOME": str(off),
                                    "XDG_CACHE_HOME": ""}, key) == size
     assert not off.exists()
+
+
+def test_python_layer_counts_planes_before_the_c_abi():
+    # the C ABI reads exactly the op's number of plane pointers: a short list
+    # from the Python layer would hand it pointers from past the array's end,
+    # so every wrapper counts first (no GPU needed: nothing reaches the C side)
+    import torch
+    t = [torch.empty(8, dtype=torch.float64) for _ in range(80)]
+    cases = [
+        lambda: fvb.flux(t[:5], 3, out=t[:14]),
+        lambda: fvb.flux_prim(t[:5], 3, out=t[:16]),
+        lambda: fvb.cons2prim(t[:5], 3, out=t[:4]),
+        lambda: fvb.prim2cons(t[:5], 3, out=t[:5]),
+        lambda: fvb.jacobian(t[:5], 3, out=t[:74]),
+        lambda: fvb.synth_state(3, 8, out=t[:4]),
+    ]
+    for call in cases:
+        with pytest.raises(fvb.ArgumentError, match="planes expected"):
+            call()
+    ctx = object.__new__(fvb.HostContext)  # no device: only the argument checks run
+    with pytest.raises(fvb.ArgumentError, match="planes expected"):
+        fvb.HostContext.flux(ctx, t[:5], 3, t[:16])
+    with pytest.raises(fvb.ArgumentError, match="planes expected"):
+        fvb.HostContext.jacobian(ctx, t[:4], 3, t[:75])

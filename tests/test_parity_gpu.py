@@ -66,6 +66,21 @@ def test_synth_state_bitwise(cuda, orc, prec, dim):
         assert all_same(to_host(dev), want)
 
 
+def test_synth_outputs_are_validated(cuda):
+    # the generators write planes of `prec`: an f32 plane (half the bytes)
+    # or a short plane under prec=1 would be an out-of-bounds device write
+    with pytest.raises(fvb.PrecisionError):
+        fvb.synth_state(3, 100, prec=1, out=[torch.empty(100, dtype=torch.float32, device=cuda)
+                                             for _ in range(5)])
+    with pytest.raises(fvb.LengthMismatch):
+        fvb.synth_state(3, 100, prec=1, out=[torch.empty(99, dtype=torch.float64, device=cuda)
+                                             for _ in range(5)])
+    with pytest.raises(fvb.PrecisionError):
+        fvb.synth_uniform(100, prec=1, out=torch.empty(100, dtype=torch.float32, device=cuda))
+    with pytest.raises(fvb.LengthMismatch):
+        fvb.synth_uniform(100, prec=0, out=torch.empty(50, dtype=torch.float32, device=cuda))
+
+
 def test_synth_uniform_bitwise(cuda, orc):
     for prec in ("f64", "f32"):
         d = fvb.synth_uniform(3000, prec=PREC[prec], seed=1, first=3000)
@@ -237,6 +252,25 @@ def test_lambda_max_output_is_validated(cuda, orc):
                        torch.cuda.current_stream().cuda_stream))
         torch.cuda.synchronize()
         assert lam.item() == 7.0
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_cfl_lambda_max_on_a_side_stream(cuda, orc, prec):
+    # shard.cfl_lambda_max with the reduction on the caller's stream: the
+    # widening copy (and, under torch.distributed, the all-reduce) on the
+    # current stream must wait for it; a torch stream and a raw handle
+    from paper_1809_09851_b200 import shard
+    dim, n = 3, 2_000_003
+    s_np = orc.random_state(dim, n, seed=21, prec=prec)
+    s = to_dev(s_np, cuda)
+    want = float(orc.wave_speed_max(dim, s_np))
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    for st in (side, side.cuda_stream):
+        with torch.cuda.stream(side):
+            torch.cuda._sleep(2_000_000)  # the reduction lands late on the side stream
+        lam = shard.cfl_lambda_max(s, dim, stream=st)
+        assert lam.dtype == torch.float64 and lam.item() == want
 
 
 def test_lambda_invariant_to_slicing(cuda, orc):
