@@ -815,7 +815,7 @@ def stencil7(n):
     return rp, cols[mask].astype(np.uint64), vals[mask].astype(np.float64)
 
 
-@pytest.fixture(params=["auto", "row", "warp"])
+@pytest.fixture(params=["auto", "row", "warp", "pipe"])
 def csr_mode(request, monkeypatch):
     # the library reads FVB_CSR_MODE per call
     if request.param != "auto":
