@@ -176,6 +176,19 @@ struct Ctx {
 
 void download(const DeviceVector& d, DenseVector& h) { d.download(h); }
 
+// The harness runs on be.ordinal and gives the caller's thread its current
+// device back on every exit.
+struct OnDevice {
+    int prev = -1;
+    explicit OnDevice(int dev) {
+        cuda_ok(cudaGetDevice(&prev), "cudaGetDevice");
+        cuda_ok(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~OnDevice() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 }  // namespace
 
 std::string bench_label(const DeviceBackend& be) {
@@ -186,7 +199,7 @@ std::vector<BenchRecord> run_micro(const BenchConfig& cfg, const DeviceBackend& 
                                    BenchPlanes where) {
     cfg.validate();
     std::vector<BenchRecord> out;
-    cuda_ok(cudaSetDevice(be.ordinal), "cudaSetDevice");
+    OnDevice on(be.ordinal);
     const cudaStream_t stream = static_cast<cudaStream_t>(be.stream);
     const uint8_t prec = cfg.precision == Precision::f64 ? FVB_F64 : FVB_F32;
 
@@ -292,7 +305,7 @@ std::vector<BenchRecord> run_miniapp(const BenchConfig& cfg, const DeviceBackend
                                      BenchPlanes where) {
     cfg.validate();
     std::vector<BenchRecord> out;
-    cuda_ok(cudaSetDevice(be.ordinal), "cudaSetDevice");
+    OnDevice on(be.ordinal);
     const cudaStream_t stream = static_cast<cudaStream_t>(be.stream);
     const uint8_t prec = cfg.precision == Precision::f64 ? FVB_F64 : FVB_F32;
 
