@@ -139,6 +139,15 @@ struct fvb_ctx {
 namespace fvb {
 namespace {
 
+// Sweep knobs of the host side (tools/gpu_e2e_jac_sweep.sh; unset = the
+// measured defaults): FVB_FILL_THREADS (host-side fills and pass-through
+// copies), FVB_POOL_THREADS (bounce and duplicate copies), FVB_DUPS_ON_LINK=1
+// (the Jacobian's duplicate entries shipped over PCIe instead of copied).
+int env_knob(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
+
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {
@@ -312,7 +321,9 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
     for (const Arg& a : args) any_dup |= a.dup_of >= 0;
     if ((any_pageable || any_dup) && !ctx->pool) {
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-        ctx->pool.reset(new (std::nothrow) CopyPool(std::min(16u, hw) - 1));
+        static const int knob = env_knob("FVB_POOL_THREADS", 0);
+        const unsigned workers = knob > 0 ? unsigned(knob) : std::min(16u, hw) - 1;
+        ctx->pool.reset(new (std::nothrow) CopyPool(workers));
     }
     auto copy = [&](const std::vector<Piece>& p) {
         if (ctx->pool)
@@ -450,7 +461,9 @@ struct HostSide {
         const size_t total = jobs.size() * bytes;
         // a thread per 1 MiB at most: a thread costs tens of microseconds to
         // start and join, so a small call writes inline (below)
-        const unsigned nt = unsigned(std::min<size_t>(std::min(8u, std::max(1u, hw / 2)),
+        static const int knob = env_knob("FVB_FILL_THREADS", 0);
+        const unsigned cap = knob > 0 ? unsigned(knob) : std::min(8u, std::max(1u, hw / 2));
+        const unsigned nt = unsigned(std::min<size_t>(cap,
                                                       std::max<size_t>(1, total >> 20)));
         const size_t per = ((total + nt - 1) / nt + 63) & ~size_t(63);  // whole elements
         auto work = [jobs, bytes](size_t lo, size_t hi) {
@@ -558,7 +571,9 @@ fvb_status pipeline(fvb_ctx* ctx, const void* const* in, void* const* out, uint6
                 host_side.push_back({static_cast<char*>(out[j]), nullptr, bits});
                 on_host = true;
             } else if (!on_host) {
-                dup = Op::duplicate_of(j);  // an earlier, computed and shipped output
+                static const bool dups_on_link = env_knob("FVB_DUPS_ON_LINK", 0) != 0;
+                if (!dups_on_link)
+                    dup = Op::duplicate_of(j);  // an earlier, computed and shipped output
             }
         }
         Arg a{on_host || dup >= 0 ? nullptr : static_cast<char*>(out[j]), nullptr, sizeof(T), true};
