@@ -602,30 +602,55 @@ struct DevBuf {
 // device planes: a bare leaf is used in place when resident (else uploaded
 // once), any other operand expression is evaluated once on the device into
 // a scratch plane -- the reference's "one scratch per distinct operand".
+// As in the reference, every operand is captured before any destination is
+// written (a snapshot: y = M * y swaps correctly), and a resident operand
+// whose plane is itself a destination is copied first, not used in place.
 void run_matvec(const DeviceBackend& be, std::vector<std::pair<const BlockItem*, Out>>& mv) {
     DeviceGuard guard(be.ordinal);
     cudaStream_t s = static_cast<cudaStream_t>(be.stream);
     std::map<const ExprNode*, std::unique_ptr<DeviceVector>> owned;
     std::map<const ExprNode*, const DeviceVector*> planes;
-    auto operand = [&](const Expr& op, std::size_t cols) -> const DeviceVector& {
+    auto is_dest_plane = [&](const DeviceVector* p) {
+        for (const auto& m : mv)
+            if (m.second.dev == p) return true;
+        return false;
+    };
+    auto capture = [&](const Expr& op, std::size_t cols) {
         const ExprNode* key = op.ptr().get();
-        auto it = planes.find(key);
-        if (it != planes.end()) return *it->second;
+        if (planes.count(key)) return;
         if (const DenseVector* lf = bare_leaf(op.node())) {
             if (lf->size() != cols)
                 throw LengthMismatch("matvec column count " + std::to_string(cols) +
                                      " vs operand length " + std::to_string(lf->size()));
-            if (DeviceVector* dv = be.residency ? be.residency->find(lf) : nullptr)
-                return *(planes[key] = dv);
+            DeviceVector* dv = be.residency ? be.residency->find(lf) : nullptr;
+            if (dv && !is_dest_plane(dv)) {
+                planes[key] = dv;
+                return;
+            }
             auto t = std::make_unique<DeviceVector>(lf->precision(), lf->size());
-            t->upload(*lf);
+            if (dv) {  // the resident plane is written by this block: a snapshot
+                if (dv->size() != lf->size() || dv->precision() != lf->precision())
+                    throw LengthMismatch("resident plane does not match its host leaf");
+                if (t->byte_size())
+                    cuda_check(cudaMemcpyAsync(t->data(), dv->data(), t->byte_size(),
+                                               cudaMemcpyDeviceToDevice, s),
+                               "matvec operand snapshot");
+            } else {
+                t->upload(*lf);
+            }
             planes[key] = t.get();
-            return *(owned[key] = std::move(t));
+            owned[key] = std::move(t);
+            return;
         }
         auto t = std::make_unique<DeviceVector>(op.result_precision(), cols);
         evaluate(be, op, *t);
         planes[key] = t.get();
-        return *(owned[key] = std::move(t));
+        owned[key] = std::move(t);
+    };
+    for (auto& [item, d] : mv)
+        for (const MatVecTerm& t : item->terms()) capture(t.operand, t.mat->cols());
+    auto operand = [&](const Expr& op) -> const DeviceVector& {
+        return *planes.at(op.ptr().get());
     };
     for (auto& [item, d] : mv) {
         const std::size_t rows = d.size();
@@ -640,7 +665,7 @@ void run_matvec(const DeviceBackend& be, std::vector<std::pair<const BlockItem*,
             if (t.mat->rows() != rows)
                 throw LengthMismatch("matvec row count " + std::to_string(t.mat->rows()) +
                                      " vs destination length " + std::to_string(rows));
-            const DeviceVector& x = operand(t.operand, t.mat->cols());
+            const DeviceVector& x = operand(t.operand);
             if (x.size() != t.mat->cols())
                 throw LengthMismatch("matvec column count " + std::to_string(t.mat->cols()) +
                                      " vs operand length " + std::to_string(x.size()));

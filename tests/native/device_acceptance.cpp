@@ -387,6 +387,73 @@ void run_gpu() {
         return "max ulp: " + report;
     });
 
+    check("matvec operands are snapshots taken before any destination is written (block.cpp:389-411)", [&] {
+        // test_block.cpp:214-230: y = [0 I; I 0] * y swaps the two vectors;
+        // also items built by hand whose later operand is an earlier
+        // destination, and resident operands whose plane is a destination
+        SplitMix64 rng(66);
+        const std::size_t n = 37;
+        std::vector<Triplet> eye;
+        for (std::size_t i = 0; i < n; ++i) eye.push_back({i, i, 1.0});
+        const SparseMatrix zero(n, n, {}), I(n, n, eye);
+        BlockMatrix swap(2, 2, zero, I, I, zero);
+        auto fresh = [&] {
+            std::vector<DenseVector> v;
+            v.push_back(testutil::make_vec(Precision::f64, n, rng, -2.0, 2.0));
+            v.push_back(testutil::make_vec(Precision::f64, n, rng, -2.0, 2.0));
+            return v;
+        };
+        {   // host vectors
+            auto v = fresh();
+            const std::vector<DenseVector> old = v;
+            BlockColVector want(std::vector<DenseVector>{v[0], v[1]}), got(std::move(v));
+            BlockExpr pw = block_matvec(swap, want), pg = block_matvec(swap, got);
+            evaluate_block(ref, pw, want);
+            dev::evaluate_block(be, pg, got);
+            if (!same_bits(got.get(0), old[1]) || !same_bits(got.get(1), old[0]) ||
+                !same_bits(got.get(0), want.get(0)) || !same_bits(got.get(1), want.get(1)))
+                fail("y = swap * y on host vectors");
+        }
+        {   // item 1 reads item 0's destination: it must see the old value
+            auto v = fresh();
+            DenseVector a = testutil::make_vec(Precision::f64, n, rng, -2.0, 2.0);
+            const DenseVector old0 = v[0];
+            BlockColVector got(std::move(v));
+            std::vector<BlockItem> items;
+            items.push_back(BlockItem(std::vector<MatVecTerm>{{&I, leaf(a)}}));
+            items.push_back(BlockItem(std::vector<MatVecTerm>{{&I, leaf(got.get(0))}}));
+            dev::evaluate_block(be, BlockExpr(2, 1, std::move(items)), got);
+            if (!same_bits(got.get(0), a) || !same_bits(got.get(1), old0))
+                fail("a later operand saw an earlier destination's new value");
+        }
+        {   // resident operands whose planes are the tie'd destinations
+            auto v = fresh();
+            const std::vector<DenseVector> old = v;
+            std::vector<dev::DeviceVector> dvs;
+            for (auto& x : v) {
+                dvs.push_back(dev::make_temp(Precision::f64, n));
+                dvs.back().upload(x);
+            }
+            dev::Residency res;
+            res.bind(v[0], dvs[0]);
+            res.bind(v[1], dvs[1]);
+            dev::DeviceBackend rb;
+            rb.residency = &res;
+            BlockColVector yv(std::vector<DenseVector>{v[0], v[1]});
+            std::vector<BlockItem> ops;
+            ops.push_back(BlockItem(leaf(v[0])));
+            ops.push_back(BlockItem(leaf(v[1])));
+            dev::evaluate_block(rb, block_matvec(swap, BlockExpr(2, 1, std::move(ops))),
+                                dev::tie(dvs[0], dvs[1]));
+            DenseVector t0(Precision::f64, n), t1(Precision::f64, n);
+            dvs[0].download(t0);
+            dvs[1].download(t1);
+            if (!same_bits(t0, old[1]) || !same_bits(t1, old[0]))
+                fail("resident operands aliasing tie'd destinations");
+        }
+        return "";
+    });
+
     check("criterion 7 on device: CSR block matvec, all shapes <= 3x3, dims <= 8, bitwise", [&] {
         // acceptance.cpp:343-379 builds random sparse blocks and compares to a
         // dense oracle within 1e-12; the device path must equal the
