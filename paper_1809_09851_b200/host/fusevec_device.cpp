@@ -605,14 +605,25 @@ struct DevBuf {
 // As in the reference, every operand is captured before any destination is
 // written (a snapshot: y = M * y swaps correctly), and a resident operand
 // whose plane is itself a destination is copied first, not used in place.
-void run_matvec(const DeviceBackend& be, std::vector<std::pair<const BlockItem*, Out>>& mv) {
-    DeviceGuard guard(be.ordinal);
-    cudaStream_t s = static_cast<cudaStream_t>(be.stream);
+struct MatvecOperands {
     std::map<const ExprNode*, std::unique_ptr<DeviceVector>> owned;
     std::map<const ExprNode*, const DeviceVector*> planes;
+    const DeviceVector& at(const Expr& op) const { return *planes.at(op.ptr().get()); }
+};
+
+// Every operand of the block's matvec rows, captured before any of the
+// block's destinations (`dests`: all of them, element-wise items' included)
+// is written.
+void capture_operands(const DeviceBackend& be,
+                      const std::vector<std::pair<const BlockItem*, Out>>& mv,
+                      const std::vector<Out>& dests, MatvecOperands& ops) {
+    DeviceGuard guard(be.ordinal);
+    cudaStream_t s = static_cast<cudaStream_t>(be.stream);
+    auto& owned = ops.owned;
+    auto& planes = ops.planes;
     auto is_dest_plane = [&](const DeviceVector* p) {
-        for (const auto& m : mv)
-            if (m.second.dev == p) return true;
+        for (const Out& o : dests)
+            if (o.dev == p) return true;
         return false;
     };
     auto capture = [&](const Expr& op, std::size_t cols) {
@@ -647,64 +658,74 @@ void run_matvec(const DeviceBackend& be, std::vector<std::pair<const BlockItem*,
         planes[key] = t.get();
         owned[key] = std::move(t);
     };
-    for (auto& [item, d] : mv)
+    for (const auto& [item, d] : mv)
         for (const MatVecTerm& t : item->terms()) capture(t.operand, t.mat->cols());
-    auto operand = [&](const Expr& op) -> const DeviceVector& {
-        return *planes.at(op.ptr().get());
-    };
-    for (auto& [item, d] : mv) {
-        const std::size_t rows = d.size();
-        std::unique_ptr<DeviceVector> tmp;
-        DeviceVector* y = d.dev;
-        if (!y) {
-            tmp = std::make_unique<DeviceVector>(d.prec(), rows);
-            y = tmp.get();
-        }
-        if (rows) cuda_check(cudaMemsetAsync(y->data(), 0, y->byte_size(), s), "matvec reset");
-        for (const MatVecTerm& t : item->terms()) {
-            if (t.mat->rows() != rows)
-                throw LengthMismatch("matvec row count " + std::to_string(t.mat->rows()) +
-                                     " vs destination length " + std::to_string(rows));
-            const DeviceVector& x = operand(t.operand);
-            if (x.size() != t.mat->cols())
-                throw LengthMismatch("matvec column count " + std::to_string(t.mat->cols()) +
-                                     " vs operand length " + std::to_string(x.size()));
-            const int py = y->precision() == Precision::f64 ? 1 : 0;
-            const int px = x.precision() == Precision::f64 ? 1 : 0;
-            if (const DeviceCsr* dm = be.residency ? be.residency->find(t.mat) : nullptr) {
-                // a resident matrix: no upload
-                if (dm->narrow_indices())
-                    fvb_check(fvb_csr_matvec_acc_u32(py, px, rows, dm->nnz(), dm->row_ptr(),
-                                                     dm->col_idx32(), dm->values(), x.data(),
-                                                     y->data(), s));
-                else
-                    fvb_check(fvb_csr_matvec_acc(py, px, rows, dm->nnz(), dm->row_ptr(),
-                                                 dm->col_idx(), dm->values(), x.data(), y->data(),
-                                                 s));
-                continue;
-            }
-            const auto& rp = t.mat->row_ptr();
-            const auto& ci = t.mat->col_idx();
-            const auto& v = t.mat->values();
-            static_assert(sizeof(std::size_t) == sizeof(uint64_t), "64-bit size_t");
-            DevBuf drp(rp.size() * 8), dci(ci.size() * 8), dv(v.size() * 8);
-            if (!rp.empty())
-                cuda_check(cudaMemcpyAsync(drp.p, rp.data(), rp.size() * 8, cudaMemcpyHostToDevice, s), "csr upload");
-            if (!ci.empty()) {
-                cuda_check(cudaMemcpyAsync(dci.p, ci.data(), ci.size() * 8, cudaMemcpyHostToDevice, s), "csr upload");
-                cuda_check(cudaMemcpyAsync(dv.p, v.data(), v.size() * 8, cudaMemcpyHostToDevice, s), "csr upload");
-            }
-            fvb_check(fvb_csr_matvec_acc(py, px, rows, ci.size(),
-                                         static_cast<const uint64_t*>(drp.p),
-                                         static_cast<const uint64_t*>(dci.p),
-                                         static_cast<const double*>(dv.p), x.data(), y->data(), s));
-            cuda_check(cudaStreamSynchronize(s), "matvec");  // before the CSR buffers go
-        }
-        cuda_check(cudaStreamSynchronize(s), "matvec");
-        if (d.host && rows)
-            cuda_check(cudaMemcpy(d.host->raw(), y->data(), y->byte_size(), cudaMemcpyDeviceToHost),
-                       "matvec read-back");
+}
+
+// One matvec row item into its destination, from captured operands.
+void run_matvec_item(const DeviceBackend& be, const BlockItem* item, const Out& d,
+                     const MatvecOperands& ops) {
+    DeviceGuard guard(be.ordinal);
+    cudaStream_t s = static_cast<cudaStream_t>(be.stream);
+    const std::size_t rows = d.size();
+    std::unique_ptr<DeviceVector> tmp;
+    DeviceVector* y = d.dev;
+    if (!y) {
+        tmp = std::make_unique<DeviceVector>(d.prec(), rows);
+        y = tmp.get();
     }
+    if (rows) cuda_check(cudaMemsetAsync(y->data(), 0, y->byte_size(), s), "matvec reset");
+    for (const MatVecTerm& t : item->terms()) {
+        if (t.mat->rows() != rows)
+            throw LengthMismatch("matvec row count " + std::to_string(t.mat->rows()) +
+                                 " vs destination length " + std::to_string(rows));
+        const DeviceVector& x = ops.at(t.operand);
+        if (x.size() != t.mat->cols())
+            throw LengthMismatch("matvec column count " + std::to_string(t.mat->cols()) +
+                                 " vs operand length " + std::to_string(x.size()));
+        const int py = y->precision() == Precision::f64 ? 1 : 0;
+        const int px = x.precision() == Precision::f64 ? 1 : 0;
+        if (const DeviceCsr* dm = be.residency ? be.residency->find(t.mat) : nullptr) {
+            // a resident matrix: no upload
+            if (dm->narrow_indices())
+                fvb_check(fvb_csr_matvec_acc_u32(py, px, rows, dm->nnz(), dm->row_ptr(),
+                                                 dm->col_idx32(), dm->values(), x.data(),
+                                                 y->data(), s));
+            else
+                fvb_check(fvb_csr_matvec_acc(py, px, rows, dm->nnz(), dm->row_ptr(),
+                                             dm->col_idx(), dm->values(), x.data(), y->data(),
+                                             s));
+            continue;
+        }
+        const auto& rp = t.mat->row_ptr();
+        const auto& ci = t.mat->col_idx();
+        const auto& v = t.mat->values();
+        static_assert(sizeof(std::size_t) == sizeof(uint64_t), "64-bit size_t");
+        DevBuf drp(rp.size() * 8), dci(ci.size() * 8), dv(v.size() * 8);
+        if (!rp.empty())
+            cuda_check(cudaMemcpyAsync(drp.p, rp.data(), rp.size() * 8, cudaMemcpyHostToDevice, s), "csr upload");
+        if (!ci.empty()) {
+            cuda_check(cudaMemcpyAsync(dci.p, ci.data(), ci.size() * 8, cudaMemcpyHostToDevice, s), "csr upload");
+            cuda_check(cudaMemcpyAsync(dv.p, v.data(), v.size() * 8, cudaMemcpyHostToDevice, s), "csr upload");
+        }
+        fvb_check(fvb_csr_matvec_acc(py, px, rows, ci.size(),
+                                     static_cast<const uint64_t*>(drp.p),
+                                     static_cast<const uint64_t*>(dci.p),
+                                     static_cast<const double*>(dv.p), x.data(), y->data(), s));
+        cuda_check(cudaStreamSynchronize(s), "matvec");  // before the CSR buffers go
+    }
+    cuda_check(cudaStreamSynchronize(s), "matvec");
+    if (d.host && rows)
+        cuda_check(cudaMemcpy(d.host->raw(), y->data(), y->byte_size(), cudaMemcpyDeviceToHost),
+                   "matvec read-back");
+}
+
+// CSR block-matvec rows of a block, operands captured first.
+void run_matvec(const DeviceBackend& be, std::vector<std::pair<const BlockItem*, Out>>& mv,
+                const std::vector<Out>& dests) {
+    MatvecOperands ops;
+    capture_operands(be, mv, dests, ops);
+    for (const auto& [item, d] : mv) run_matvec_item(be, item, d, ops);
 }
 
 void leaves_of(const ExprNode& n, std::vector<const DenseVector*>& out) {
@@ -916,6 +937,7 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
     std::vector<Out> outs;
     std::vector<std::pair<const DenseVector*, Out>> copies;  // bare-leaf items
     std::vector<std::pair<const BlockItem*, Out>> matvecs;   // CSR block-matvec rows
+    std::vector<std::pair<bool, std::size_t>> order;  // (matvec?, index): the reference's item order
     std::size_t idx = 0;
     for (std::size_t r = 0; r < rows; ++r)
         for (std::size_t c = 0; c < cols; ++c, ++idx) {
@@ -926,6 +948,7 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
                 case ItemKind::Vector: x = leaf(it.vector()); break;
                 case ItemKind::MatVec:
                     if (need_reduce) throw UnsupportedExpression("matvec block has no CFL reduction");
+                    order.push_back({true, matvecs.size()});
                     matvecs.push_back({&it, dests_in[idx]});
                     continue;
                 default:  // as the reference: proj/src/block.cpp:427-428
@@ -936,6 +959,7 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
             validate(x.node(), d.size(), tags);
             // aliased pass-through moves no memory (proj/src/block.cpp:419-422)
             if (d.host && bare_leaf(x.node()) == d.host) continue;
+            order.push_back({false, items.size()});
             items.push_back(x);
             outs.push_back(d);
         }
@@ -947,31 +971,45 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
     // Two items writing one destination: the later one's value stands, as
     // item-by-item evaluation leaves it (the host-buffer pipeline refuses
     // one plane named for two outputs).
-    if (!hazard && !need_reduce && matvecs.empty()) {
+    // (Matvec rows count too: with them the order decides which value stands.)
+    if (!hazard && !need_reduce) {
         std::unordered_map<const void*, int> seen;
-        for (const Out& o : outs)
-            if ((o.host || o.dev) &&
-                ++seen[o.host ? static_cast<const void*>(o.host) : o.dev] > 1)
-                hazard = true;
+        auto twice = [&](const Out& o) {
+            return (o.host || o.dev) &&
+                   ++seen[o.host ? static_cast<const void*>(o.host) : o.dev] > 1;
+        };
+        for (const Out& o : outs) hazard = twice(o) || hazard;
+        for (const auto& m : matvecs) hazard = twice(m.second) || hazard;
     }
-    if (hazard && (need_reduce || !matvecs.empty()))
+    if (hazard && need_reduce)
         throw UnsupportedExpression(
-            "block whose destinations alias operands of its own items (CFL or matvec block)");
-    // Matvec rows first: their operands are captured before any destination
-    // of this block is written (the reference's scratch pass, block.cpp:389-411).
-    if (!matvecs.empty()) run_matvec(be, matvecs);
+            "CFL block whose destinations alias operands of its own items");
+    if (hazard) {
+        // The reference's own order (block.cpp:389-451): every matvec operand
+        // captured first, then the items one by one, so an item reading an
+        // earlier item's destination sees the new values and a later one's
+        // the old.
+        MatvecOperands ops;
+        if (!matvecs.empty()) capture_operands(be, matvecs, dests_in, ops);
+        for (const auto& [is_mv, k] : order) {
+            if (is_mv) {
+                run_matvec_item(be, matvecs[k].first, matvecs[k].second, ops);
+                continue;
+            }
+            Plan one;
+            if (!try_plan({items[k]}, {outs[k]}, 1, 1, &one)) unsupported({items[k]});
+            run(be, one, outs[k].size(), nullptr);
+        }
+        return;
+    }
+    // Matvec rows first: no element-wise item reads their destinations (no
+    // hazard), and their operands are captured before any destination of this
+    // block is written (the reference's scratch pass, block.cpp:389-411).
+    if (!matvecs.empty()) run_matvec(be, matvecs, dests_in);
     if (items.empty()) return;
     const std::size_t n = outs[0].size();
     for (const Out& o : outs)
         if (o.size() != n) throw LengthMismatch("block destinations have different lengths");
-    if (hazard) {
-        for (std::size_t i = 0; i < items.size(); ++i) {
-            Plan one;
-            if (!try_plan({items[i]}, {outs[i]}, 1, 1, &one)) unsupported({items[i]});
-            run(be, one, n, nullptr);
-        }
-        return;
-    }
     // Matvec rows or aliased pass-throughs were taken out: the fused key
     // covers the remaining element-wise items as one column.
     if (items.size() != rows * cols) {

@@ -454,6 +454,49 @@ void run_gpu() {
         return "";
     });
 
+    check("blocks mixing matvec rows and element-wise items that read each other's destinations", [&] {
+        // block.cpp:389-451: operands captured first, then items in order --
+        // an element-wise item after a matvec row reads its new value, one
+        // before it the old
+        SplitMix64 rng(77);
+        const std::size_t n = 29;
+        std::vector<Triplet> trips;
+        for (std::size_t r = 0; r < n; ++r)
+            for (std::size_t c = 0; c < n; ++c)
+                if (rng.uniform() < 0.3) trips.push_back({r, c, rng.uniform(-2.0, 2.0)});
+        const SparseMatrix M(n, n, trips);
+        auto vec = [&] { return testutil::make_vec(Precision::f64, n, rng, -2.0, 2.0); };
+        DenseVector x = vec();
+        for (int variant = 0; variant < 3; ++variant) {
+            std::vector<DenseVector> init{vec(), vec(), vec()};
+            BlockColVector want{std::vector<DenseVector>(init)}, got{std::vector<DenseVector>(init)};
+            auto build = [&](BlockColVector& y) {
+                std::vector<BlockItem> it;
+                const Expr two = constant(2.0, Precision::f64);
+                if (variant == 0) {  // after: item 1 reads the matvec's new d0
+                    it.push_back(BlockItem(std::vector<MatVecTerm>{{&M, leaf(x)}}));
+                    it.push_back(BlockItem(leaf(y.get(0)) * two));
+                    it.push_back(BlockItem(leaf(y.get(2)) + leaf(x)));
+                } else if (variant == 1) {  // before: item 0 reads d1's old value
+                    it.push_back(BlockItem(leaf(y.get(1)) * two));
+                    it.push_back(BlockItem(std::vector<MatVecTerm>{{&M, leaf(y.get(0))}}));
+                    it.push_back(BlockItem(leaf(y.get(1)) - leaf(x)));
+                } else {  // a later item reading an element-wise and a matvec destination
+                    it.push_back(BlockItem(leaf(x) * two));
+                    it.push_back(BlockItem(std::vector<MatVecTerm>{{&M, leaf(x)}}));
+                    it.push_back(BlockItem(leaf(y.get(0)) + leaf(y.get(1))));
+                }
+                return BlockExpr(3, 1, std::move(it));
+            };
+            evaluate_block(ref, build(want), want);
+            dev::evaluate_block(be, build(got), got);
+            for (std::size_t i = 0; i < 3; ++i)
+                if (!same_bits(got.get(i), want.get(i)))
+                    fail("variant " + std::to_string(variant) + " item " + std::to_string(i));
+        }
+        return "";
+    });
+
     check("criterion 7 on device: CSR block matvec, all shapes <= 3x3, dims <= 8, bitwise", [&] {
         // acceptance.cpp:343-379 builds random sparse blocks and compares to a
         // dense oracle within 1e-12; the device path must equal the
