@@ -260,6 +260,44 @@ void add_pieces(std::vector<Piece>& v, char* dst, const char* src, size_t bytes)
         v.push_back({dst + at, src + at, std::min(kPiece, bytes - at)});
 }
 
+// Copies between a slot's device staging and its pinned bounce buffer, one
+// per run of planes that sit back to back in both layouts (in a pageable
+// call usually all inputs in one run and all outputs in another) instead of
+// one per plane: a small chunk costs a few microseconds per copy call.  A run
+// also moves the unused tails of its inner planes (chunk - cnt elements),
+// which stay inside both buffers and are never read.
+struct BounceRuns {
+    struct Run {
+        size_t dev0, pin0, dev1, pin1, last_width;  // offsets in bytes per point
+    };
+    std::vector<Run> v;
+    void add(size_t dev_off, size_t pin_off, size_t width) {
+        if (!v.empty() && v.back().dev1 == dev_off && v.back().pin1 == pin_off) {
+            v.back().dev1 += width;
+            v.back().pin1 += width;
+            v.back().last_width = width;
+            return;
+        }
+        v.push_back({dev_off, pin_off, dev_off + width, pin_off + width, width});
+    }
+    fvb_status flush(char* dbase, char* pin, uint64_t chunk, uint64_t cnt, cudaMemcpyKind kind,
+                     cudaStream_t s) {
+        for (const Run& r : v) {
+            const size_t bytes = (r.dev1 - r.last_width - r.dev0) * chunk + cnt * r.last_width;
+            char* d = dbase + r.dev0 * chunk;
+            char* h = pin + r.pin0 * chunk;
+            const cudaError_t e = kind == cudaMemcpyHostToDevice
+                                      ? cudaMemcpyAsync(d, h, bytes, kind, s)
+                                      : cudaMemcpyAsync(h, d, bytes, kind, s);
+            if (e != cudaSuccess)
+                return cuda_fail(e, kind == cudaMemcpyHostToDevice ? "host->device copy"
+                                                                   : "device->host copy");
+        }
+        v.clear();
+        return FVB_OK;
+    }
+};
+
 // The staged executor.  `launch(dev_args, cnt, stream)` enqueues the kernel
 // for one chunk; dev_args follow `args` (device pointers at the chunk, NULL
 // for NULL slots).  Returns once every output is in place.
@@ -370,6 +408,7 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
     };
 
     std::vector<void*> dargs(args.size());
+    BounceRuns runs;
     for (uint64_t c = 0; c < nchunks; ++c) {
         const int slot = int(c % fvb_ctx::kSlots);
         cudaStream_t s = ctx->stream[slot];
@@ -404,22 +443,32 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
             }
             dargs[i] = dbase + a.dev_off * chunk;
             if (a.out) continue;
-            const char* src = a.has_pin ? pin + a.pin_off * chunk : a.host + off * a.width;
-            const cudaError_t e =
-                cudaMemcpyAsync(dargs[i], src, cnt * a.width, cudaMemcpyHostToDevice, s);
+            if (a.has_pin) {
+                runs.add(a.dev_off, a.pin_off, a.width);
+                continue;
+            }
+            const cudaError_t e = cudaMemcpyAsync(dargs[i], a.host + off * a.width,
+                                                  cnt * a.width, cudaMemcpyHostToDevice, s);
             if (e != cudaSuccess) return cuda_fail(e, "host->device copy");
         }
+        if (fvb_status st = runs.flush(dbase, pin, chunk, cnt, cudaMemcpyHostToDevice, s))
+            return st;
         if (fvb_status st = launch(dargs.data(), cnt, s)) return st;
         bool unpack = false;
         for (size_t i = 0; i < args.size(); ++i) {
             const Arg& a = args[i];
             if (!a.out || !a.host) continue;
-            char* dst = a.has_pin ? pin + a.pin_off * chunk : a.host + off * a.width;
             unpack |= a.has_pin;
-            const cudaError_t e =
-                cudaMemcpyAsync(dst, dargs[i], cnt * a.width, cudaMemcpyDeviceToHost, s);
+            if (a.has_pin) {
+                runs.add(a.dev_off, a.pin_off, a.width);
+                continue;
+            }
+            const cudaError_t e = cudaMemcpyAsync(a.host + off * a.width, dargs[i], cnt * a.width,
+                                                  cudaMemcpyDeviceToHost, s);
             if (e != cudaSuccess) return cuda_fail(e, "device->host copy");
         }
+        if (fvb_status st = runs.flush(dbase, pin, chunk, cnt, cudaMemcpyDeviceToHost, s))
+            return st;
         if (unpack || any_dup || packed) {
             const cudaError_t e = cudaEventRecord(ctx->done[slot], s);
             if (e != cudaSuccess) return cuda_fail(e, "chunk event");
