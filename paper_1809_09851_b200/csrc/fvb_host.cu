@@ -266,6 +266,30 @@ void add_pieces(std::vector<Piece>& v, char* dst, const char* src, size_t bytes)
 // one per plane: a small chunk costs a few microseconds per copy call.  A run
 // also moves the unused tails of its inner planes (chunk - cnt elements),
 // which stay inside both buffers and are never read.
+// One direction's copies of a chunk, issued together after the loop that
+// collects them (one cudaMemcpyAsync each).
+struct CopyBatch {
+    std::vector<void*> dst, src;
+    std::vector<size_t> bytes;
+    void add(void* d, const void* s, size_t b) {
+        dst.push_back(d);
+        src.push_back(const_cast<void*>(s));
+        bytes.push_back(b);
+    }
+    fvb_status flush(cudaMemcpyKind kind, cudaStream_t s) {
+        for (size_t i = 0; i < dst.size(); ++i) {
+            const cudaError_t e = cudaMemcpyAsync(dst[i], src[i], bytes[i], kind, s);
+            if (e != cudaSuccess)
+                return cuda_fail(e, kind == cudaMemcpyHostToDevice ? "host->device copy"
+                                                                   : "device->host copy");
+        }
+        dst.clear();
+        src.clear();
+        bytes.clear();
+        return FVB_OK;
+    }
+};
+
 struct BounceRuns {
     struct Run {
         size_t dev0, pin0, dev1, pin1, last_width;  // offsets in bytes per point
@@ -280,21 +304,18 @@ struct BounceRuns {
         }
         v.push_back({dev_off, pin_off, dev_off + width, pin_off + width, width});
     }
-    fvb_status flush(char* dbase, char* pin, uint64_t chunk, uint64_t cnt, cudaMemcpyKind kind,
-                     cudaStream_t s) {
+    void flush(char* dbase, char* pin, uint64_t chunk, uint64_t cnt, cudaMemcpyKind kind,
+               CopyBatch& out) {
         for (const Run& r : v) {
             const size_t bytes = (r.dev1 - r.last_width - r.dev0) * chunk + cnt * r.last_width;
             char* d = dbase + r.dev0 * chunk;
             char* h = pin + r.pin0 * chunk;
-            const cudaError_t e = kind == cudaMemcpyHostToDevice
-                                      ? cudaMemcpyAsync(d, h, bytes, kind, s)
-                                      : cudaMemcpyAsync(h, d, bytes, kind, s);
-            if (e != cudaSuccess)
-                return cuda_fail(e, kind == cudaMemcpyHostToDevice ? "host->device copy"
-                                                                   : "device->host copy");
+            if (kind == cudaMemcpyHostToDevice)
+                out.add(d, h, bytes);
+            else
+                out.add(h, d, bytes);
         }
         v.clear();
-        return FVB_OK;
     }
 };
 
@@ -409,6 +430,7 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
 
     std::vector<void*> dargs(args.size());
     BounceRuns runs;
+    CopyBatch copies;
     for (uint64_t c = 0; c < nchunks; ++c) {
         const int slot = int(c % fvb_ctx::kSlots);
         cudaStream_t s = ctx->stream[slot];
@@ -447,12 +469,17 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
                 runs.add(a.dev_off, a.pin_off, a.width);
                 continue;
             }
+            if (a.pinned) {
+                copies.add(dargs[i], a.host + off * a.width, cnt * a.width);
+                continue;
+            }
+            // pageable without bounce buffers: the driver stages it
             const cudaError_t e = cudaMemcpyAsync(dargs[i], a.host + off * a.width,
                                                   cnt * a.width, cudaMemcpyHostToDevice, s);
             if (e != cudaSuccess) return cuda_fail(e, "host->device copy");
         }
-        if (fvb_status st = runs.flush(dbase, pin, chunk, cnt, cudaMemcpyHostToDevice, s))
-            return st;
+        runs.flush(dbase, pin, chunk, cnt, cudaMemcpyHostToDevice, copies);
+        if (fvb_status st = copies.flush(cudaMemcpyHostToDevice, s)) return st;
         if (fvb_status st = launch(dargs.data(), cnt, s)) return st;
         bool unpack = false;
         for (size_t i = 0; i < args.size(); ++i) {
@@ -463,12 +490,16 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
                 runs.add(a.dev_off, a.pin_off, a.width);
                 continue;
             }
+            if (a.pinned) {
+                copies.add(a.host + off * a.width, dargs[i], cnt * a.width);
+                continue;
+            }
             const cudaError_t e = cudaMemcpyAsync(a.host + off * a.width, dargs[i], cnt * a.width,
                                                   cudaMemcpyDeviceToHost, s);
             if (e != cudaSuccess) return cuda_fail(e, "device->host copy");
         }
-        if (fvb_status st = runs.flush(dbase, pin, chunk, cnt, cudaMemcpyDeviceToHost, s))
-            return st;
+        runs.flush(dbase, pin, chunk, cnt, cudaMemcpyDeviceToHost, copies);
+        if (fvb_status st = copies.flush(cudaMemcpyDeviceToHost, s)) return st;
         if (unpack || any_dup || packed) {
             const cudaError_t e = cudaEventRecord(ctx->done[slot], s);
             if (e != cudaSuccess) return cuda_fail(e, "chunk event");
