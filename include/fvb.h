@@ -283,7 +283,8 @@ FVB_API fvb_status fvb_ctx_destroy(fvb_ctx* ctx);
  * in chunks with host->device copies, the fused kernel and device->host
  * copies overlapped on separate streams; returns after the last byte is
  * back in host memory.  lambda_max is a HOST double.  A device pointer
- * among the host planes is refused (FVB_EARG) before anything runs. */
+ * among the host planes is refused (FVB_EARG), and so is a host plane that
+ * is not element-aligned (FVB_EALIGN), before anything runs. */
 FVB_API fvb_status fvb_flux_host(fvb_ctx* ctx, const fvb_gas* gas, uint32_t dim, uint8_t prec,
                          uint64_t n, const void* const* in, void* const* out);
 FVB_API fvb_status fvb_jacobian_host(fvb_ctx* ctx, const fvb_gas* gas, uint32_t dim, uint8_t prec,

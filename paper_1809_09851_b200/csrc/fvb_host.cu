@@ -230,10 +230,13 @@ Mem memory_kind(const void* p) {
 // Host threads write (and read) host planes before staged() classifies
 // them, so a device pointer handed over as a host plane is refused first:
 // on the host it would be a wild access, not an error code.
-fvb_status host_planes(const void* const* p, size_t count) {
-    for (size_t i = 0; i < count; ++i)
+fvb_status host_planes(const void* const* p, size_t count, size_t width) {
+    for (size_t i = 0; i < count; ++i) {
+        if (p[i] && reinterpret_cast<uintptr_t>(p[i]) % width)
+            return fail(FVB_EALIGN, "host plane is not element-aligned");
         if (p[i] && memory_kind(p[i]) == Mem::kDevice)
             return fail(FVB_EARG, "a host plane is device memory");
+    }
     return FVB_OK;
 }
 
@@ -621,8 +624,9 @@ fvb_status pipeline(fvb_ctx* ctx, const void* const* in, void* const* out, uint6
             return fail(FVB_EARG, "two host outputs name one plane");
     }
     DeviceGuard guard(ctx->device);
-    if (fvb_status st = host_planes(in, NIN)) return st;
-    if (fvb_status st = host_planes(const_cast<const void* const*>(out), NOUT)) return st;
+    if (fvb_status st = host_planes(in, NIN, sizeof(T))) return st;
+    if (fvb_status st = host_planes(const_cast<const void* const*>(out), NOUT, sizeof(T)))
+        return st;
     using Bu = typename Bits<T>::U;
     if (RED)
         if (fvb_status st = reset_lambda(ctx, sizeof(Bu))) return st;
@@ -885,7 +889,8 @@ fvb_status fvb_launch_host(fvb_ctx* ctx, const fvb_kernel* k, uint64_t n, void* 
         }
         DeviceGuard guard(ctx->device);
         for (const Arg& a : v)
-            if (fvb_status st = host_planes(reinterpret_cast<const void* const*>(&a.host), 1))
+            if (fvb_status st =
+                    host_planes(reinterpret_cast<const void* const*>(&a.host), 1, a.width))
                 return st;
         const size_t red_bytes = k->prec ? 8 : 4;  // the kernel's accumulator
         if (lambda_max)

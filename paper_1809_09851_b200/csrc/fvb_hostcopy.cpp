@@ -46,6 +46,10 @@ void plain_fill(char* d, uint64_t bits, size_t width, size_t n) {
 }
 
 __attribute__((target("avx2"))) void stream_fill(char* d, uint64_t bits, size_t width, size_t n) {
+    if (reinterpret_cast<uintptr_t>(d) % width) {  // the vector pattern needs element alignment
+        plain_fill(d, bits, width, n);
+        return;
+    }
     size_t head = (32 - (reinterpret_cast<uintptr_t>(d) & 31)) & 31;  // a multiple of width
     if (head > n) head = n;
     plain_fill(d, bits, width, head);

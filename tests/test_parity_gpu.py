@@ -489,6 +489,16 @@ def test_host_path_refuses_device_planes_before_host_threads(cuda, orc):
                                      (ctypes.c_uint8 * count)(*([1] * count)),
                                      (ctypes.c_uint8 * count)(*([0] * count)), None, None)
         assert st == N.FVB_EARG and b"device memory" in N.lib().fvb_last_error()
+    # a host plane that is not element-aligned (host threads fill and copy
+    # element-wise): refused with FVB_EALIGN
+    raw = torch.empty(n * 8 + 8, dtype=torch.uint8)
+    odd = raw.data_ptr() + 4
+    outs = [torch.empty(n, dtype=torch.float64) for _ in range(15)]
+    ptrs = [t.data_ptr() for t in outs]
+    ptrs[3] = odd
+    st = N.lib().fvb_flux_host(ctx._h, None, 3, 1, n, N.ptr_array([t.data_ptr() for t in hs]),
+                               N.ptr_array(ptrs))
+    assert st == N.FVB_EALIGN
     # the context still works afterwards
     s_np = orc.random_state(3, n, seed=11)
     fo = [torch.empty(n, dtype=torch.float64) for _ in range(15)]
