@@ -142,8 +142,13 @@ fvb_status fvb_synth_state(uint32_t dim, uint8_t prec, uint64_t seed, uint64_t f
     if (fvb_status st = check_common(dim, prec)) return st;
     if (n == 0) return FVB_OK;
     if (!out) return fail(FVB_EARG, "NULL plane array");
-    for (uint32_t i = 0; i < dim + 2; ++i)
+    const size_t w = prec == FVB_F64 ? 8 : 4;
+    for (uint32_t i = 0; i < dim + 2; ++i) {
         if (!out[i]) return fail(FVB_EARG, "NULL output plane");
+        // a misaligned store would be a sticky device fault, not an error code
+        if (reinterpret_cast<uintptr_t>(out[i]) % w)
+            return fail(FVB_EALIGN, "output plane is not element-aligned");
+    }
     auto s = static_cast<cudaStream_t>(stream);
     const unsigned grid = simple_grid(n);
     auto go = [&](auto tag, auto dtag) {
@@ -172,6 +177,8 @@ fvb_status fvb_synth_uniform(uint8_t prec, uint64_t seed, uint64_t first, uint64
     if (fvb_status st = check_common(1, prec, false)) return st;
     if (n == 0) return FVB_OK;
     if (!out) return fail(FVB_EARG, "NULL plane");
+    if (reinterpret_cast<uintptr_t>(out) % (prec == FVB_F64 ? 8 : 4))
+        return fail(FVB_EALIGN, "output plane is not element-aligned");
     auto s = static_cast<cudaStream_t>(stream);
     if (prec == FVB_F64)
         synth_uniform_kernel<double><<<simple_grid(n), 256, 0, s>>>(seed, first, n, lo, hi,

@@ -282,6 +282,12 @@ fvb_status csr_entry(uint8_t prec_y, uint8_t prec_x, uint64_t rows, uint64_t nnz
     if (rows == 0) return FVB_OK;
     if (!row_ptr || !y || (nnz && (!col_idx || !values || !x)))
         return fail(FVB_EARG, "NULL CSR array or plane");
+    // misaligned loads or stores would be a sticky device fault, not an error code
+    auto misaligned = [](const void* p, size_t w) { return reinterpret_cast<uintptr_t>(p) % w != 0; };
+    if (misaligned(row_ptr, 8) || misaligned(y, prec_y ? 8 : 4) ||
+        (nnz && (misaligned(col_idx, sizeof(IT)) || misaligned(values, 8) ||
+                 misaligned(x, prec_x ? 8 : 4))))
+        return fail(FVB_EALIGN, "CSR array or plane is not element-aligned");
     auto s = static_cast<cudaStream_t>(stream);
     if (prec_y == FVB_F64)
         return prec_x == FVB_F64

@@ -81,6 +81,28 @@ def test_synth_outputs_are_validated(cuda):
         fvb.synth_uniform(100, prec=0, out=torch.empty(50, dtype=torch.float32, device=cuda))
 
 
+def test_misaligned_device_planes_refused_before_launch(cuda, orc):
+    # a misaligned plane would be a sticky device fault (the context dies):
+    # the generators and the CSR accumulation refuse it with FVB_EALIGN, and
+    # the device keeps working afterwards
+    raw = torch.empty(8 * 1000 + 8, dtype=torch.uint8, device=cuda)
+    odd = raw.data_ptr() + 4
+    planes = [torch.empty(1000, dtype=torch.float64, device=cuda) for _ in range(5)]
+    ptrs = [t.data_ptr() for t in planes]
+    ptrs[2] = odd
+    assert N.lib().fvb_synth_state(3, 1, 5, 0, 1000, N.ptr_array(ptrs), None) == N.FVB_EALIGN
+    assert N.lib().fvb_synth_uniform(1, 5, 0, 1000, 0.0, 1.0, odd, None) == N.FVB_EALIGN
+    rp, ci, v = stencil7(5)
+    drp, dci, dv = _csr_to_dev(rp, ci, v, cuda)
+    x = torch.zeros(len(rp) - 1, dtype=torch.float64, device=cuda)
+    st = N.lib().fvb_csr_matvec_acc(1, 1, len(rp) - 1, len(ci), drp.data_ptr(), dci.data_ptr(),
+                                    dv.data_ptr(), x.data_ptr(), odd, None)
+    assert st == N.FVB_EALIGN
+    torch.cuda.synchronize()
+    s = fvb.synth_state(3, 1000)
+    assert all_same(to_host(s), orc.random_state(3, 1000, seed=0x5EED))
+
+
 def test_synth_uniform_bitwise(cuda, orc):
     for prec in ("f64", "f32"):
         d = fvb.synth_uniform(3000, prec=PREC[prec], seed=1, first=3000)
