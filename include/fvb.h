@@ -168,7 +168,10 @@ FVB_API fvb_status fvb_wave_speed_max(const fvb_gas* gas, uint32_t dim, uint8_t 
  * (bitwise the reference's order).  row_ptr (rows+1 entries), col_idx and
  * values (nnz entries, already narrowed to the matrix precision as
  * SparseMatrix stores them) are DEVICE arrays; x and y device planes of
- * precisions prec_x / prec_y. */
+ * precisions prec_x / prec_y.  The arrays must form a valid CSR matrix, as
+ * SparseMatrix guarantees (row_ptr non-decreasing from 0 to nnz, every
+ * column index inside x): the device does not re-check the structure.
+ * NULL or misaligned arrays are refused (FVB_EARG / FVB_EALIGN). */
 FVB_API fvb_status fvb_csr_matvec_acc(uint8_t prec_y, uint8_t prec_x, uint64_t rows, uint64_t nnz,
                                       const uint64_t* row_ptr, const uint64_t* col_idx,
                                       const double* values, const void* x, void* y,
