@@ -19,7 +19,7 @@ write per item.  That is 528 B/pt for the 3-D flux, against the fused kernel's
 160 algorithmic B/pt, which the JSON records separately.  For device rows,
 overhead_ratio = device time / HBM-roofline time at the measured copy peak.
 For the reference's own record it is its generic/hand-fused ratio.  N = 2e9
-fp64 needs 320 GB and so >= 2 GPUs; it is listed as infeasible at G = 1.
+fp64 needs 320 GB and so >= 2 GPUs; it is listed as infeasible at G = 1 (f32, 160 GB, runs).
 """
 
 import argparse
@@ -70,8 +70,11 @@ def main():
     R = oracle.reference()
     threads = len(os.sched_getaffinity(0))
     sizes = [int(10 ** e) for e in range(3, 10) if 10 ** e <= a.max]
-    for extra in (int(5e8),):
-        if extra <= a.max:
+    # 5e8, and 2e9 where its 20 planes fit this GPU (f32: 160 GB of 180;
+    # f64 needs 320 GB, i.e. >= 2 GPUs)
+    free = torch.cuda.mem_get_info()[0]
+    for extra in (int(5e8), int(2e9)):
+        if extra <= a.max and (extra < int(2e9) or 20 * w * extra < free - (2 << 30)):
             sizes.append(extra)
     sizes = sorted(set(sizes))
     recs, csv = [], []
@@ -140,8 +143,10 @@ def main():
                        f"{tflops * n / med_c / 1e6:.3f},{tbytes * n / med_c / 1e6:.3f},nan")
         recs.append(rec)
         print(json.dumps(rec), flush=True)
-    recs.append({"n": 2_000_000_000, "prec": a.prec, "gpus": 1,
-                 "infeasible": "needs 320 GB of planes (fp64): >= 2 GPUs"})
+    if int(2e9) not in sizes:
+        recs.append({"n": 2_000_000_000, "prec": a.prec, "gpus": 1,
+                     "infeasible": f"needs {20 * w * 2} GB of planes ({a.prec}): more than one "
+                                   f"GPU's {free / 1e9:.0f} GB free"})
     if R is not None:
         med_ns, ratio = R.run_miniapp(a.prec, 1 << 24, threads)
         csv.append(f"miniapp,parallel,{a.prec},{1 << 24},{med_ns:.3f},"
