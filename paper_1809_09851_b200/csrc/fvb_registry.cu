@@ -26,6 +26,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "fvb.h"
@@ -500,6 +501,12 @@ bool match(const std::string& pat, const char* key, double* consts, bool* seen) 
 }  // namespace
 }  // namespace fvb
 
+namespace fvb {
+namespace {
+fvb_status lookup_uncached(const char* key, fvb_kernel* out);
+}  // namespace
+}  // namespace fvb
+
 using namespace fvb;
 
 extern "C" {
@@ -507,6 +514,37 @@ extern "C" {
 fvb_status fvb_lookup(const char* key, fvb_kernel* out) {
     return guarded([&]() -> fvb_status {
         if (!key || !out) return fail(FVB_EARG, "NULL key or output");
+        // Resolved keys, for the process lifetime like the reference's JIT
+        // cache (backend_jit.cpp:240-253): a repeated key -- every call of a
+        // time loop that rebuilds its trees -- costs one hash lookup instead
+        // of a scan of the patterns.
+        static std::mutex mu;
+        static std::unordered_map<std::string, fvb_kernel> resolved;
+        const std::string k_text(key);
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            auto it = resolved.find(k_text);
+            if (it != resolved.end()) {
+                *out = it->second;
+                return FVB_OK;
+            }
+        }
+        const fvb_status st = lookup_uncached(key, out);
+        if (st == FVB_OK) {
+            std::lock_guard<std::mutex> lock(mu);
+            resolved.emplace(k_text, *out);
+        }
+        return st;
+    });
+}
+
+}  // extern "C"
+
+namespace fvb {
+namespace {
+
+fvb_status lookup_uncached(const char* key, fvb_kernel* out) {
+    {
         // FVB_FORCE_LOWER=1 skips the hand-written kernels (tests and the
         // hand-written-vs-lowered comparison run the same trees both ways).
         static const bool force_lower = [] {
@@ -545,8 +583,13 @@ fvb_status fvb_lookup(const char* key, fvb_kernel* out) {
         }
         // No hand-written kernel: lower the tree itself (NVRTC, cached per key).
         return lower_lookup(key, out);
-    });
+    }
 }
+
+}  // namespace
+}  // namespace fvb
+
+extern "C" {
 
 uint32_t fvb_pattern_count(void) {
     try {
