@@ -136,43 +136,75 @@ struct Slots {
     }
 };
 
-// Small appenders for the key text (a 75-item Jacobian key is ~4 KB, built
-// on every evaluate_block call).
-void append_uint(std::string& out, std::size_t v) {
-    char buf[24];
-    int i = 0;
-    do {
-        buf[i++] = char('0' + v % 10);
-        v /= 10;
-    } while (v);
-    while (i) out += buf[--i];
-}
-
-void append_hex16(std::string& out, unsigned long long bits) {
-    static const char kHex[] = "0123456789abcdef";
-    char buf[16];
-    for (int i = 15; i >= 0; --i, bits >>= 4) buf[i] = kHex[bits & 15];
-    out.append(buf, 16);
-}
+// The key text is written through a raw cursor into a string grown ahead
+// in large steps (a 75-item Jacobian key is ~4.4 KB, built on every
+// evaluate_block call whose trees are not reused): no per-character
+// capacity checks.
+struct KeyOut {
+    std::string& s;
+    char* p;
+    char* end;
+    explicit KeyOut(std::string& str) : s(str) {
+        const std::size_t used = s.size();
+        s.resize(std::max<std::size_t>(used + 1024, 2 * used));
+        p = &s[0] + used;
+        end = &s[0] + s.size();
+    }
+    // the slow path, out of line: the string doubles
+    __attribute__((noinline)) void grow(std::size_t k) {
+        const std::size_t used = std::size_t(p - &s[0]);
+        s.resize(std::max(2 * s.size(), used + k + 1024));
+        p = &s[0] + used;
+        end = &s[0] + s.size();
+    }
+    char* room(std::size_t k) {
+        if (std::size_t(end - p) < k) grow(k);
+        char* q = p;
+        p += k;
+        return q;
+    }
+    void put(char c) { *room(1) = c; }
+    void uint(std::size_t v) {
+        if (v < 10) {
+            put(char('0' + v));
+            return;
+        }
+        char buf[24];
+        int i = 0;
+        do {
+            buf[i++] = char('0' + v % 10);
+            v /= 10;
+        } while (v);
+        char* q = room(std::size_t(i));
+        while (i) *q++ = buf[--i];
+    }
+    void hex16(unsigned long long bits) {
+        static const char kHex[] = "0123456789abcdef";
+        char* q = room(16);
+        for (int i = 15; i >= 0; --i, bits >>= 4) q[i] = kHex[bits & 15];
+    }
+    void finish() { s.resize(std::size_t(p - &s[0])); }
+};
 
 // key_node (proj/src/backend_jit.cpp:112-155): same grammar, same order.
-void key_node(const ExprNode& n, Slots& slots, bool& ok, std::string& out) {
+void key_node(const ExprNode& n, Slots& slots, bool& ok, KeyOut& out) {
     switch (n.kind) {
-        case NodeKind::Leaf:
-            out += 'L';
-            out += prec_char(n.prec);
-            append_uint(out, slots.of(n.vec));
-            out += ';';
+        case NodeKind::Leaf: {
+            out.put('L');
+            out.put(prec_char(n.prec));
+            out.uint(slots.of(n.vec));
+            out.put(';');
             return;
+        }
         case NodeKind::Constant: {
             const double v = narrow(n.value, n.prec);
             if (!std::isfinite(v)) ok = false;
             unsigned long long bits;
             std::memcpy(&bits, &v, sizeof bits);
-            out += 'C';
-            out += prec_char(n.prec);
-            append_hex16(out, bits);
-            out += ';';
+            out.put('C');
+            out.put(prec_char(n.prec));
+            out.hex16(bits);
+            out.put(';');
             return;
         }
         case NodeKind::Tagged:
@@ -180,24 +212,30 @@ void key_node(const ExprNode& n, Slots& slots, bool& ok, std::string& out) {
             key_node(*n.left, slots, ok, out);
             return;
         case NodeKind::Unary:
-            out += 'U';
-            append_uint(out, static_cast<std::size_t>(n.uop));
-            out += prec_char(n.prec);
-            out += '(';
+            out.put('U');
+            out.uint(static_cast<std::size_t>(n.uop));
+            out.put(prec_char(n.prec));
+            out.put('(');
             key_node(*n.left, slots, ok, out);
-            out += ')';
+            out.put(')');
             return;
         case NodeKind::Binary:
-            out += 'B';
-            append_uint(out, static_cast<std::size_t>(n.bop));
-            out += prec_char(n.prec);
-            out += '(';
+            out.put('B');
+            out.uint(static_cast<std::size_t>(n.bop));
+            out.put(prec_char(n.prec));
+            out.put('(');
             key_node(*n.left, slots, ok, out);
-            out += ',';
+            out.put(',');
             key_node(*n.right, slots, ok, out);
-            out += ')';
+            out.put(')');
             return;
     }
+}
+
+void key_node(const ExprNode& n, Slots& slots, bool& ok, std::string& out) {
+    KeyOut w(out);
+    key_node(n, slots, ok, w);
+    w.finish();
 }
 
 // validate() semantics of proj/src/backend_eval.cpp:236-265.
@@ -751,28 +789,33 @@ bool reads_earlier_destination(const DeviceBackend& be, const std::vector<Expr>&
     // plane that is some leaf's resident copy); matvec rows count as written
     // before every item.  Linear in the leaves, so a 75-item Jacobian block
     // costs one pass over its trees.
-    std::unordered_map<const void*, long> writer;
+    // (address, earliest writing item) sorted by address: a block has at most
+    // a few hundred destinations, so a binary search beats hashing here
+    std::vector<std::pair<const void*, long>> writer;
+    writer.reserve(matvecs.size() + outs.size());
     for (const auto& mv : matvecs) {
         const Out& o = mv.second;
-        if (o.host || o.dev) writer[o.host ? static_cast<const void*>(o.host) : o.dev] = -1;
+        if (o.host || o.dev) writer.push_back({o.host ? static_cast<const void*>(o.host) : o.dev, -1});
     }
     for (std::size_t j = 0; j < outs.size(); ++j) {
         const Out& o = outs[j];
         if (o.host || o.dev)
-            writer.emplace(o.host ? static_cast<const void*>(o.host) : o.dev, long(j));
+            writer.push_back({o.host ? static_cast<const void*>(o.host) : o.dev, long(j)});
     }
     if (writer.empty()) return false;
+    std::sort(writer.begin(), writer.end());  // equal addresses: the earliest writer first
+    auto earliest = [&](const void* p) -> long {
+        auto it = std::lower_bound(writer.begin(), writer.end(), std::make_pair(p, long(-2)));
+        return it != writer.end() && it->first == p ? it->second : long(items.size());
+    };
     std::vector<const DenseVector*> ls;
     for (std::size_t k = 0; k < items.size(); ++k) {
         ls.clear();
         leaves_of(items[k].node(), ls);
         for (const DenseVector* l : ls) {
-            auto it = writer.find(l);
-            if (it != writer.end() && it->second < long(k)) return true;
-            if (const DeviceVector* dv = be.residency ? be.residency->find(l) : nullptr) {
-                it = writer.find(dv);
-                if (it != writer.end() && it->second < long(k)) return true;
-            }
+            if (earliest(l) < long(k)) return true;
+            if (const DeviceVector* dv = be.residency ? be.residency->find(l) : nullptr)
+                if (earliest(dv) < long(k)) return true;
         }
     }
     return false;
@@ -973,13 +1016,15 @@ void block_impl(const DeviceBackend& be, const BlockExpr& e, std::size_t rows, s
     // one plane named for two outputs).
     // (Matvec rows count too: with them the order decides which value stands.)
     if (!hazard && !need_reduce) {
-        std::unordered_map<const void*, int> seen;
-        auto twice = [&](const Out& o) {
-            return (o.host || o.dev) &&
-                   ++seen[o.host ? static_cast<const void*>(o.host) : o.dev] > 1;
+        std::vector<const void*> seen;
+        seen.reserve(outs.size() + matvecs.size());
+        auto note = [&](const Out& o) {
+            if (o.host || o.dev) seen.push_back(o.host ? static_cast<const void*>(o.host) : o.dev);
         };
-        for (const Out& o : outs) hazard = twice(o) || hazard;
-        for (const auto& m : matvecs) hazard = twice(m.second) || hazard;
+        for (const Out& o : outs) note(o);
+        for (const auto& m : matvecs) note(m.second);
+        std::sort(seen.begin(), seen.end());
+        hazard = std::adjacent_find(seen.begin(), seen.end()) != seen.end();
     }
     if (hazard && need_reduce)
         throw UnsupportedExpression(
@@ -1336,12 +1381,13 @@ std::string block_key(const std::vector<Expr>& items, const std::vector<Precisio
     Slots slots;
     bool ok = true;
     std::string key = "G" + std::to_string(rows) + "x" + std::to_string(cols) + ":";
-    key.reserve(items.size() * 64);
+    KeyOut w(key);
     for (std::size_t i = 0; i < items.size(); ++i) {
-        if (i) key += '|';
-        key += prec_char(dests[i]);
-        key_node(items[i].node(), slots, ok, key);
+        if (i) w.put('|');
+        w.put(prec_char(dests[i]));
+        key_node(items[i].node(), slots, ok, w);
     }
+    w.finish();
     if (leaves) *leaves = slots.v;
     return ok ? key : std::string();
 }
