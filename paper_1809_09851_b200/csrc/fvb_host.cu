@@ -5,7 +5,7 @@
 // The reference evaluates host DenseVectors in place (proj/src/
 // backend_eval.cpp:280-346).  A drop-in device backend handed host buffers
 // must move them over PCIe; this path hides the kernel behind the copies.
-// The range is cut into chunks, and chunk c runs on slot c % kSlots as
+// The range is cut into chunks, and chunk c runs on slot c % slots as
 // [H2D inputs -> fused kernel -> D2H outputs] in that slot's stream, so the
 // H2D of one chunk, the kernel of another and the D2H of a third overlap on
 // the two copy directions.
@@ -122,14 +122,15 @@ class CopyPool {
 }  // namespace fvb
 
 struct fvb_ctx {
-    static constexpr int kSlots = 3;
+    static constexpr int kMaxSlots = 8;
+    int slots = 3;  // pipeline depth (FVB_HOST_SLOTS, 2..8; a sweep knob)
     int device = 0;
     uint64_t chunk_points = 0;  // 0 = size chunks by bytes
-    cudaStream_t stream[kSlots] = {};
-    cudaEvent_t done[kSlots] = {};  // the slot's last D2H has completed
-    void* slot_buf[kSlots] = {};    // device staging
+    cudaStream_t stream[kMaxSlots] = {};
+    cudaEvent_t done[kMaxSlots] = {};  // the slot's last D2H has completed
+    void* slot_buf[kMaxSlots] = {};    // device staging
     size_t slot_bytes = 0;
-    void* pin_buf[kSlots] = {};     // pinned bounce buffers for pageable planes
+    void* pin_buf[kMaxSlots] = {};     // pinned bounce buffers for pageable planes
     size_t pin_bytes = 0;
     void* red = nullptr;            // lambda-max accumulator (8 bytes)
     cudaEvent_t reset_done = nullptr;
@@ -165,27 +166,27 @@ struct DeviceGuard {
 fvb_status ensure_buffers(fvb_ctx* ctx, size_t dev_bytes, size_t pin_bytes, bool* pinned) {
     *pinned = true;
     if (dev_bytes > ctx->slot_bytes || pin_bytes > ctx->pin_bytes) {
-        for (int s = 0; s < fvb_ctx::kSlots; ++s) cudaStreamSynchronize(ctx->stream[s]);
+        for (int s = 0; s < ctx->slots; ++s) cudaStreamSynchronize(ctx->stream[s]);
     }
     if (dev_bytes > ctx->slot_bytes) {
-        for (int s = 0; s < fvb_ctx::kSlots; ++s) {
+        for (int s = 0; s < ctx->slots; ++s) {
             if (ctx->slot_buf[s]) cudaFree(ctx->slot_buf[s]);
             ctx->slot_buf[s] = nullptr;
         }
         ctx->slot_bytes = 0;
-        for (int s = 0; s < fvb_ctx::kSlots; ++s) {
+        for (int s = 0; s < ctx->slots; ++s) {
             const cudaError_t e = cudaMalloc(&ctx->slot_buf[s], dev_bytes);
             if (e != cudaSuccess) return cuda_fail(e, "staging allocation");
         }
         ctx->slot_bytes = dev_bytes;
     }
     if (pin_bytes > ctx->pin_bytes) {
-        for (int s = 0; s < fvb_ctx::kSlots; ++s) {
+        for (int s = 0; s < ctx->slots; ++s) {
             if (ctx->pin_buf[s]) cudaFreeHost(ctx->pin_buf[s]);
             ctx->pin_buf[s] = nullptr;
         }
         ctx->pin_bytes = 0;
-        for (int s = 0; s < fvb_ctx::kSlots; ++s) {
+        for (int s = 0; s < ctx->slots; ++s) {
             if (cudaHostAlloc(&ctx->pin_buf[s], pin_bytes, cudaHostAllocDefault) != cudaSuccess) {
                 cudaGetLastError();  // not sticky: fall back to unbounced copies
                 for (int q = 0; q <= s; ++q) {
@@ -399,11 +400,11 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
     struct Drain {
         fvb_ctx* ctx;
         ~Drain() {
-            for (int s = 0; s < fvb_ctx::kSlots; ++s) cudaStreamSynchronize(ctx->stream[s]);
+            for (int s = 0; s < ctx->slots; ++s) cudaStreamSynchronize(ctx->stream[s]);
         }
     } drain{ctx};
     const uint64_t nchunks = (n + chunk - 1) / chunk;
-    int64_t pending[fvb_ctx::kSlots];
+    int64_t pending[fvb_ctx::kMaxSlots];
     for (auto& p : pending) p = -1;
     std::vector<Piece> pieces;
     // Unpack the pageable outputs of the chunk a slot last carried.
@@ -435,7 +436,7 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
     BounceRuns runs;
     CopyBatch copies;
     for (uint64_t c = 0; c < nchunks; ++c) {
-        const int slot = int(c % fvb_ctx::kSlots);
+        const int slot = int(c % ctx->slots);
         cudaStream_t s = ctx->stream[slot];
         const uint64_t off = c * chunk;
         const uint64_t cnt = std::min(chunk, n - off);
@@ -509,9 +510,9 @@ fvb_status staged(fvb_ctx* ctx, std::vector<Arg>& args, uint64_t n, Launch&& lau
             pending[slot] = int64_t(c);
         }
     }
-    for (uint64_t c = nchunks > fvb_ctx::kSlots ? nchunks - fvb_ctx::kSlots : 0; c < nchunks; ++c)
-        if (fvb_status st = finish(int(c % fvb_ctx::kSlots))) return st;
-    for (int s = 0; s < fvb_ctx::kSlots; ++s) {
+    for (uint64_t c = nchunks > ctx->slots ? nchunks - ctx->slots : 0; c < nchunks; ++c)
+        if (fvb_status st = finish(int(c % ctx->slots))) return st;
+    for (int s = 0; s < ctx->slots; ++s) {
         const cudaError_t e = cudaStreamSynchronize(ctx->stream[s]);
         if (e != cudaSuccess) return cuda_fail(e, "pipeline completion");
     }
@@ -544,8 +545,12 @@ struct HostSide {
         const size_t total = jobs.size() * bytes;
         // a thread per 1 MiB at most: a thread costs tens of microseconds to
         // start and join, so a small call writes inline (below)
+        // four threads by default (a quarter of a 16-core host): more copy
+        // threads slow the concurrent DMA into host memory more than they
+        // gain (A/B on two boxes, profiles/r02_e2e_fill_threads_ab.jsonl:
+        // flux e2e -2.4..-3.4%, Jacobian e2e -2..-5% with 8 threads)
         static const int knob = env_knob("FVB_FILL_THREADS", 0);
-        const unsigned cap = knob > 0 ? unsigned(knob) : std::min(8u, std::max(1u, hw / 2));
+        const unsigned cap = knob > 0 ? unsigned(knob) : std::min(4u, std::max(2u, hw / 4));
         const unsigned nt = unsigned(std::min<size_t>(cap,
                                                       std::max<size_t>(1, total >> 20)));
         const size_t per = ((total + nt - 1) / nt + 63) & ~size_t(63);  // whole elements
@@ -584,7 +589,7 @@ struct HostSide {
 fvb_status reset_lambda(fvb_ctx* ctx, size_t bytes) {
     cudaError_t e = cudaMemsetAsync(ctx->red, 0, bytes, ctx->stream[0]);
     if (e == cudaSuccess) e = cudaEventRecord(ctx->reset_done, ctx->stream[0]);
-    for (int s = 1; s < fvb_ctx::kSlots && e == cudaSuccess; ++s)
+    for (int s = 1; s < ctx->slots && e == cudaSuccess; ++s)
         e = cudaStreamWaitEvent(ctx->stream[s], ctx->reset_done, 0);
     return e == cudaSuccess ? FVB_OK : cuda_fail(e, "lambda reset");
 }
@@ -777,8 +782,10 @@ fvb_status fvb_ctx_create(int device, uint64_t chunk_points, fvb_ctx** out) {
     if (!ctx) return fail(FVB_EHOST, "out of host memory");
     ctx->device = device;
     ctx->chunk_points = chunk_points;
+    static const int slots = env_knob("FVB_HOST_SLOTS", 3);
+    ctx->slots = std::min(fvb_ctx::kMaxSlots, std::max(2, slots));
     DeviceGuard guard(device);
-    for (int s = 0; s < fvb_ctx::kSlots && e == cudaSuccess; ++s) {
+    for (int s = 0; s < ctx->slots && e == cudaSuccess; ++s) {
         e = cudaStreamCreateWithFlags(&ctx->stream[s], cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->done[s], cudaEventDisableTiming);
     }
@@ -795,7 +802,7 @@ fvb_status fvb_ctx_create(int device, uint64_t chunk_points, fvb_ctx** out) {
 fvb_status fvb_ctx_destroy(fvb_ctx* ctx) {
     if (!ctx) return FVB_OK;
     DeviceGuard guard(ctx->device);
-    for (int s = 0; s < fvb_ctx::kSlots; ++s) {
+    for (int s = 0; s < ctx->slots; ++s) {
         if (ctx->stream[s]) cudaStreamSynchronize(ctx->stream[s]);
         if (ctx->slot_buf[s]) cudaFree(ctx->slot_buf[s]);
         if (ctx->pin_buf[s]) cudaFreeHost(ctx->pin_buf[s]);
@@ -897,7 +904,7 @@ fvb_status fvb_launch_host(fvb_ctx* ctx, const fvb_kernel* k, uint64_t n, void* 
             if (fvb_status st = reset_lambda(ctx, red_bytes)) return st;
         if (after) {  // device work the caller queued first (producing resident planes)
             cudaError_t e = cudaEventRecord(ctx->reset_done, static_cast<cudaStream_t>(after));
-            for (int s = 0; s < fvb_ctx::kSlots && e == cudaSuccess; ++s)
+            for (int s = 0; s < ctx->slots && e == cudaSuccess; ++s)
                 e = cudaStreamWaitEvent(ctx->stream[s], ctx->reset_done, 0);
             if (e != cudaSuccess) return cuda_fail(e, "ordering after the caller's stream");
         }
