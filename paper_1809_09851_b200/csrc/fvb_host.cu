@@ -264,12 +264,6 @@ void add_pieces(std::vector<Piece>& v, char* dst, const char* src, size_t bytes)
         v.push_back({dst + at, src + at, std::min(kPiece, bytes - at)});
 }
 
-// Copies between a slot's device staging and its pinned bounce buffer, one
-// per run of planes that sit back to back in both layouts (in a pageable
-// call usually all inputs in one run and all outputs in another) instead of
-// one per plane: a small chunk costs a few microseconds per copy call.  A run
-// also moves the unused tails of its inner planes (chunk - cnt elements),
-// which stay inside both buffers and are never read.
 // One direction's copies of a chunk, issued together after the loop that
 // collects them (one cudaMemcpyAsync each).
 struct CopyBatch {
@@ -294,6 +288,12 @@ struct CopyBatch {
     }
 };
 
+// Copies between a slot's device staging and its pinned bounce buffer, one
+// per run of planes that sit back to back in both layouts (in a pageable
+// call usually all inputs in one run and all outputs in another) instead of
+// one per plane: a small chunk costs a few microseconds per copy call.  A run
+// also moves the unused tails of its inner planes (chunk - cnt elements),
+// which stay inside both buffers and are never read.
 struct BounceRuns {
     struct Run {
         size_t dev0, pin0, dev1, pin1, last_width;  // offsets in bytes per point
