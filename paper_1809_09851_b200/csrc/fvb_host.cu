@@ -543,12 +543,12 @@ struct HostSide {
         if (jobs.empty() || bytes == 0) return;
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         const size_t total = jobs.size() * bytes;
-        // a thread per 1 MiB at most: a thread costs tens of microseconds to
-        // start and join, so a small call writes inline (below)
-        // four threads by default (a quarter of a 16-core host): more copy
+        // Four threads by default (a quarter of a 16-core host): more copy
         // threads slow the concurrent DMA into host memory more than they
         // gain (A/B on two boxes, profiles/r02_e2e_fill_threads_ab.jsonl:
-        // flux e2e -2.4..-3.4%, Jacobian e2e -2..-5% with 8 threads)
+        // 8 threads cost the flux e2e 2.4-3.4% and the Jacobian's 2-5%).
+        // At most one thread per MiB: starting and joining one costs tens of
+        // microseconds, so a small call writes inline (below).
         static const int knob = env_knob("FVB_FILL_THREADS", 0);
         const unsigned cap = knob > 0 ? unsigned(knob) : std::min(4u, std::max(2u, hw / 4));
         const unsigned nt = unsigned(std::min<size_t>(cap,
