@@ -21,6 +21,7 @@
 #include <cstring>
 #include <functional>
 #include <chrono>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
@@ -247,6 +248,90 @@ void run_gpu() {
                       ratio[0], ratio[1], gate, mini[0], mini[1]);
         if (ratio[0] > gate || ratio[1] > gate) fail(buf);
         return std::string(buf);
+    });
+
+    check("criterion 4 on device: backend equivalence on random trees (acceptance.cpp:161-205)", [&] {
+        // The reference's criterion: TreeGen trees of depth 5 with tagged
+        // leaves over mixed f32/f64 pools of lengths 1, 2, 257 and 1024
+        // (tree t on length t % 4), each evaluated by two backends.  Here the
+        // device backend against scalar_ref: trees of exact ops bit for bit,
+        // trees with libm nodes within rtol 1e-3 on every element of these
+        // short vectors (a few-ulp libm difference, propagated).  1000 trees
+        // as in the reference with FVB_ACC_C4_TREES=1000 (every distinct
+        // tree is one NVRTC compile; the default keeps the suite short).
+        const std::size_t lens[4] = {1, 2, 257, 1024};
+        std::vector<std::vector<DenseVector>> pools(4);
+        SplitMix64 seed_rng(0xACCE55);
+        for (int k = 0; k < 4; ++k) {
+            pools[k].push_back(testutil::make_vec(Precision::f64, lens[k], seed_rng));
+            pools[k].push_back(testutil::make_vec(Precision::f32, lens[k], seed_rng));
+            pools[k].push_back(testutil::make_vec(Precision::f64, lens[k], seed_rng));
+        }
+        const char* nt = std::getenv("FVB_ACC_C4_TREES");
+        const int trees = nt && *nt ? std::atoi(nt) : 120;
+        SplitMix64 rng(0xE0E0);
+        int exact = 0, approx = 0, constant = 0;
+        for (int t = 0; t < trees; ++t) {
+            const int k = t % 4;
+            const std::size_t n = lens[k];
+            testutil::TreeGen gen{&pools[k], true};
+            Expr e = gen.gen(rng, 5);
+            const Precision P = e.result_precision();
+            DenseVector want(P, n), got(P, n);
+            evaluate(ref, e, want);
+            try {
+                dev::evaluate(be, e, got);
+            } catch (const UnsupportedExpression&) {
+                // a leafless tree with a non-finite constant: the reference's
+                // JIT refuses it too (backend_jit.cpp:323-334)
+                ++constant;
+                continue;
+            }
+            const std::string key = dev::structural_key(e, P);
+            bool lib = false;
+            for (std::size_t i = 0; i + 1 < key.size(); ++i) {
+                if (key[i] != 'U' && key[i] != 'B') continue;
+                char* end = nullptr;
+                const long op = std::strtol(key.c_str() + i + 1, &end, 10);
+                if (!end || (*end != 's' && *end != 'd')) continue;
+                lib = lib || (key[i] == 'U' ? ((op >= 2 && op <= 14) || op == 16 || op == 20)
+                                            : (op == 4 || op == 7));
+            }
+            if (!lib) {
+                ++exact;
+                if (!same_bits(want, got)) fail("tree " + std::to_string(t) + " differs bitwise: " +
+                                                key.substr(0, 120));
+                continue;
+            }
+            ++approx;
+            for (std::size_t i = 0; i < n; ++i)
+                if (!testutil::scalar_close(want.at(i), got.at(i), 1e-3) &&
+                    !(std::isnan(want.at(i)) && std::isnan(got.at(i))))
+                    fail("tree " + std::to_string(t) + " element " + std::to_string(i) + ": " +
+                         std::to_string(want.at(i)) + " vs " + std::to_string(got.at(i)) + " " +
+                         key.substr(0, 120));
+        }
+        return std::to_string(trees) + " trees (lengths 1/2/257/1024, tagged leaves, depth 5): " +
+               std::to_string(exact) + " exact-op trees bitwise, " + std::to_string(approx) +
+               " libm trees within rtol 1e-3" +
+               (constant ? ", " + std::to_string(constant) + " refused as non-finite constants"
+                         : std::string());
+    });
+
+    check("criterion 8 on device: the benchmark CSV emitter (acceptance.cpp:404-421)", [&] {
+        BenchConfig cfg;
+        cfg.suite = "micro";
+        cfg.sizes = {1024};
+        cfg.reps = 3;
+        auto recs = dev::run_micro(cfg, be);
+        std::ostringstream os;
+        write_csv(recs, os);
+        const std::string text = os.str();
+        if (text.find("suite,backend,precision,n,median_ns,mflops,bandwidth_mbs,overhead_ratio\n") ==
+            std::string::npos)
+            fail("CSV header missing");
+        if (text.find("micro,b200x1,f64,1024,") == std::string::npos) fail("CSV row missing");
+        return "the reference's write_csv over device records: header and micro,b200x1,f64,1024 row";
     });
 
     check("general lowering: random trees (the reference's TreeGen) vs scalar_ref", [&] {

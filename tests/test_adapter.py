@@ -30,7 +30,7 @@ def test_reference_trees_resolve_to_fused_kernels():
 @pytest.mark.gpu
 def test_reference_api_on_device(cuda):
     out = run("gpu")
-    assert out.count("[PASS]") == 29
+    assert out.count("[PASS]") == 31
 
 
 @pytest.mark.gpu
@@ -40,7 +40,7 @@ def test_reference_api_on_device_all_lowered(cuda, monkeypatch):
     # hand-written kernels: still bitwise against the reference engine.
     monkeypatch.setenv("FVB_FORCE_LOWER", "1")
     out = run("gpu")
-    assert out.count("[PASS]") == 29
+    assert out.count("[PASS]") == 31
 
 
 def test_adapter_compiles_in_the_references_own_namespace():
