@@ -1,0 +1,31 @@
+#!/bin/bash
+# Builds build/integrated_api: the reference patched per INTEGRATION.md §1-3
+# (a scratch copy outside this repository, tests/native/integrate_reference.py),
+# compiled in its own namespace together with the adapter and linked with
+# libfvb.so.  Objects only land in build/integrated/.
+set -e
+HERE="$(cd "$(dirname "$0")" && pwd)"
+ROOT="$(cd "$HERE/../.." && pwd)"
+REF="${REF:-/root/reference/proj}"
+CUDA="${CUDA:-/usr/local/cuda}"
+SCRATCH="$(mktemp -d /tmp/fvb_integrated.XXXXXX)"
+trap 'rm -rf "$SCRATCH"' EXIT
+python3 "$HERE/integrate_reference.py" "$REF" "$SCRATCH"
+OUT="$HERE/build/integrated"
+mkdir -p "$OUT"
+CXXFLAGS="-std=c++20 -O3 -DNDEBUG -ffp-contract=off -fPIC -pthread -I$SCRATCH/include -I$ROOT/include \
+  -I$ROOT/paper_1809_09851_b200/host -I$CUDA/include"
+OBJS=()
+PIDS=()
+for f in "$SCRATCH"/src/*.cpp "$ROOT/paper_1809_09851_b200/host/fusevec_device.cpp" \
+         "$ROOT/paper_1809_09851_b200/host/fusevec_device_bench.cpp"; do
+  o="$OUT/$(basename "${f%.cpp}").o"
+  g++ $CXXFLAGS -I"$SCRATCH/src" -c "$f" -o "$o" &
+  PIDS+=($!)
+  OBJS+=("$o")
+done
+for p in "${PIDS[@]}"; do wait "$p"; done  # set -e: any failed compile stops the build
+g++ $CXXFLAGS -Wall -o "$HERE/build/integrated_api" "$HERE/integrated_api.cpp" "${OBJS[@]}" \
+  -L"$ROOT/paper_1809_09851_b200/lib" -lfvb -L"$CUDA/lib64" -lcudart \
+  -Wl,-rpath,'$ORIGIN/../../../paper_1809_09851_b200/lib' -Wl,-rpath,"$CUDA/lib64" -ldl -pthread
+echo "built $HERE/build/integrated_api"

@@ -97,3 +97,19 @@ def test_reference_bench_rejects_bad_config(cuda):
     p = subprocess.run([BENCH, "micro", "--sizes", "4096,1024"], capture_output=True, text=True,
                        timeout=120)
     assert p.returncode == 1 and "increasing" in p.stderr
+
+
+INTEGRATED = os.path.join(ROOT, "tests", "native", "build", "integrated_api")
+
+
+@pytest.mark.gpu
+def test_reference_with_the_integration_hook_routes_backend_device(cuda):
+    # INTEGRATION.md §1-3 applied to a copy of the reference: its own
+    # evaluate / evaluate_block with Backend::device() run the device path,
+    # bitwise against Backend::scalar_ref() (sin within 4 ulp)
+    if not os.path.exists(INTEGRATED):
+        pytest.skip("tests/native/build/integrated_api not built")
+    p = subprocess.run([INTEGRATED], capture_output=True, text=True, timeout=600)
+    print(p.stdout)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "[FAIL]" not in p.stdout and p.stdout.count("[PASS]") == 9
