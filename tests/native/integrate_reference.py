@@ -71,6 +71,19 @@ def main():
                    "        return;\n"
                    "    }\n")
 
+    # §8 (optional): the reference's own benchmark harness on the new kind
+    # (bench.cpp:34-44) -- run_micro / run_miniapp then time Backend::device()
+    # against their CPU hand-fused loops and keep their own checks (bitwise
+    # generic == hand for micro, the flux oracle and device == parallel
+    # bitwise for miniapp)
+    bn = os.path.join(dst, "src", "bench.cpp")
+    edit(bn, 'const char* backend_label(BackendKind k) {\n',
+         'const char* backend_label(BackendKind k) {\n'
+         '    if (k == BackendKind::Device) return "b200x1";\n')
+    edit(bn, 'Backend pick_backend(const BenchConfig& cfg) {\n',
+         'Backend pick_backend(const BenchConfig& cfg) {\n'
+         '    if (cfg.backend == BackendKind::Device) return Backend::device();\n')
+
 
 if __name__ == "__main__":
     main()

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "fusevec/backend.hpp"
+#include "fusevec/bench.hpp"
 #include "fusevec/block.hpp"
 #include "fusevec/fluid.hpp"
 #include "fusevec/rng.hpp"
@@ -168,6 +169,28 @@ int main() {
         }
         if (caught != 2) fail("errors not raised");
         return "LengthMismatch, TagConflict";
+    });
+    check("the reference's own run_micro / run_miniapp with BenchConfig::backend = Device", [&] {
+        // its harness keeps its own checks: micro bitwise generic == hand-fused
+        // loop, miniapp the flux oracle and device == parallel bit for bit
+        // (bench.cpp:172-176, 321-345); overhead_ratio here is the device call
+        // over the reference's single-thread CPU loop
+        std::string out;
+        for (const char* suite : {"micro", "miniapp"}) {
+            BenchConfig cfg;
+            cfg.suite = suite;
+            cfg.backend = BackendKind::Device;
+            cfg.sizes = {1024, 65536, 1u << 20};
+            cfg.reps = 3;
+            const auto recs = std::string(suite) == "micro" ? run_micro(cfg) : run_miniapp(cfg);
+            for (const auto& r : recs) {
+                if (r.backend != "b200x1") fail("backend label " + r.backend);
+                char buf[96];
+                std::snprintf(buf, sizeof buf, "%s n=%zu %.3g; ", suite, r.n, r.overhead_ratio);
+                out += buf;
+            }
+        }
+        return "device / CPU hand-fused time: " + out;
     });
     std::printf(failures ? "%d check(s) failed\n" : "all checks passed\n", failures);
     return failures ? 1 : 0;

@@ -112,4 +112,4 @@ def test_reference_with_the_integration_hook_routes_backend_device(cuda):
     p = subprocess.run([INTEGRATED], capture_output=True, text=True, timeout=600)
     print(p.stdout)
     assert p.returncode == 0, p.stdout + p.stderr
-    assert "[FAIL]" not in p.stdout and p.stdout.count("[PASS]") == 9
+    assert "[FAIL]" not in p.stdout and p.stdout.count("[PASS]") == 10
