@@ -29,6 +29,11 @@ def edit(path, old, new):
 
 def main():
     src, dst = sys.argv[1], sys.argv[2]
+    # --scalar-ref-switch (test builds only): Backend::scalar_ref() returns
+    # the device backend when FUSEVEC_SCALAR_REF_IS_DEVICE is set, so the
+    # reference's own unit tests -- and every implicit DenseVector = Expr
+    # evaluation -- run on the device unchanged
+    switch = "--scalar-ref-switch" in sys.argv[3:]
     if os.path.exists(dst):
         shutil.rmtree(dst)
     for sub in ("include", "src"):
@@ -45,6 +50,13 @@ def main():
          "        return b;\n"
          "    }\n\n"
          "    BackendKind kind() const { return kind_; }")
+    if switch:
+        edit(inc, "#include <cstddef>\n", "#include <cstddef>\n#include <cstdlib>\n")
+        edit(inc, "    static Backend scalar_ref() { return Backend(BackendKind::ScalarRef); }",
+             "    static Backend scalar_ref() {\n"
+             "        static const bool dev = std::getenv(\"FUSEVEC_SCALAR_REF_IS_DEVICE\") != nullptr;\n"
+             "        return dev ? device() : Backend(BackendKind::ScalarRef);\n"
+             "    }")
     # §2: evaluate routes the device kind after validate() (backend_eval.cpp:280-346)
     ev = os.path.join(dst, "src", "backend_eval.cpp")
     edit(ev, '#include "fusevec/backend.hpp"\n',
