@@ -57,6 +57,14 @@ for f in "$REF"/tests/doctest_main.cpp "$REF"/tests/test_*.cpp; do
   OBJS2+=("$o")
 done
 for p in "${PIDS[@]}"; do wait "$p"; done
+# and the reference's acceptance criteria (proj/tests/acceptance.cpp) on the same build
+g++ $CXX2 -I"$REF/tests" -DFUSEVEC_TEST_DIR="\"$REF/tests\"" -c "$REF/tests/acceptance.cpp" \
+  -o "$OUT2/acceptance.o"
+LIBOBJS=()
+for o in "${OBJS2[@]}"; do case "$o" in */t_*) ;; *) LIBOBJS+=("$o");; esac; done
+g++ -pthread -o "$HERE/build/reference_acceptance" "$OUT2/acceptance.o" "${LIBOBJS[@]}" \
+  -L"$ROOT/paper_1809_09851_b200/lib" -lfvb -L"$CUDA/lib64" -lcudart \
+  -Wl,-rpath,'$ORIGIN/../../../paper_1809_09851_b200/lib' -Wl,-rpath,"$CUDA/lib64" -ldl
 g++ -pthread -o "$HERE/build/reference_unit_tests" "${OBJS2[@]}" \
   -L"$ROOT/paper_1809_09851_b200/lib" -lfvb -L"$CUDA/lib64" -lcudart \
   -Wl,-rpath,'$ORIGIN/../../../paper_1809_09851_b200/lib' -Wl,-rpath,"$CUDA/lib64" -ldl

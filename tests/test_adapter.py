@@ -164,3 +164,18 @@ def test_reference_unit_tests_with_scalar_ref_on_the_device(cuda):
     passed, failed = run_units({"FUSEVEC_SCALAR_REF_IS_DEVICE": "1"})
     assert failed <= DEVICE_EXPECTED, failed - DEVICE_EXPECTED
     assert len(passed) >= 77
+
+
+ACCEPT = os.path.join(ROOT, "tests", "native", "build", "reference_acceptance")
+
+
+def test_reference_acceptance_passes_with_the_integration_hook():
+    # the reference's own 8 acceptance criteria (proj/tests/acceptance.cpp)
+    # against the reference with INTEGRATION.md §1-3 applied, CPU backends
+    if not os.path.exists(ACCEPT):
+        pytest.skip("tests/native/build/reference_acceptance not built")
+    if not os.path.isdir("/root/reference/proj/tests/golden"):
+        pytest.skip("criterion 3 reads the reference's golden file")
+    p = subprocess.run([ACCEPT], capture_output=True, text=True, timeout=600)
+    print(p.stdout)
+    assert p.returncode == 0 and "all acceptance criteria passed" in p.stdout, p.stdout + p.stderr
